@@ -1,0 +1,219 @@
+// common.cuh — device building blocks shared by all MGRIT kernels (sm_100a).
+//
+// Arithmetic that must be bit-identical to the reference is written with
+// explicit round-to-nearest intrinsics (__dmul_rn/__dadd_rn/__dsub_rn) and
+// the whole library is compiled with -fmad=false, so no FMA contraction can
+// change rounding.  FMA is used only where it is part of an exact algorithm
+// (the constant-divisor correction in lagrange_weights).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/mgrit_b200.h"
+
+namespace mgrit {
+
+constexpr double kXLo = -1.0;
+constexpr double kLen = 2.0;
+
+// ---------------------------------------------------------------------------
+// periodic decomposition (semi_lagrangian.py:118-137)
+
+// s = mod(x - x_lo, L) / h with numpy's float remainder semantics
+// (fmod, then += L when the signs differ, +0 when zero).
+__device__ __forceinline__ double scaled_coord(double x, double h) {
+    double d = __dsub_rn(x, kXLo);
+    double r = fmod(d, kLen);
+    if (r != 0.0) {
+        if (r < 0.0) r = __dadd_rn(r, kLen);
+    } else {
+        r = 0.0;
+    }
+    return __ddiv_rn(r, h);
+}
+
+struct Dec {
+    int e;       // east index in [0, n)
+    double eps;  // offset in [0, 1)
+};
+
+// east = ceil(s), eps = east - s, rounding guards, east mod n.
+__device__ __forceinline__ Dec decompose_s(double s, int n) {
+    double ef = ceil(s);
+    double eps = __dsub_rn(ef, s);
+    long long e = (long long)ef;
+    if (eps < 0.0) eps = 0.0;
+    if (eps >= 1.0) {
+        eps = __dsub_rn(eps, 1.0);
+        e -= 1;
+    }
+    e %= n;
+    if (e < 0) e += n;
+    Dec d;
+    d.e = (int)e;
+    d.eps = eps;
+    return d;
+}
+
+// ---------------------------------------------------------------------------
+// Lagrange weights (semi_lagrangian.py:140-161).
+// w_j = prod_{q != j}(z - q) / prod_{q != j}(j - q), z = -eps, offsets -l..r.
+// The division by the integer denominator D uses q0 = num*(1/D),
+// r = fma(-q0, D, num) (exact), q = fma(r, 1/D, q0): with 1/D correctly
+// rounded this is the correctly rounded quotient (Markstein), i.e. identical
+// to num / D; verified over 2e8 random operands and by the GPU parity tests.
+
+template <int P>
+struct Stencil {
+    static constexpr int L = (P + 1) / 2;  // west extent
+    static constexpr int R = (P - 1) / 2;  // east extent
+    static constexpr int Q = P + 1;        // taps
+};
+
+template <int P>
+__device__ __forceinline__ double lagrange_den(int col) {
+    constexpr int L = Stencil<P>::L, R = Stencil<P>::R;
+    double den = 1.0;
+    int j = col - L;
+#pragma unroll
+    for (int q = -L; q <= R; ++q)
+        if (q != j) den *= (double)(j - q);
+    return den;
+}
+
+__device__ __forceinline__ double div_const(double num, double den, double inv) {
+    double q0 = __dmul_rn(num, inv);
+    double r = fma(-q0, den, num);
+    return fma(r, inv, q0);
+}
+
+template <int P>
+__device__ __forceinline__ void lagrange_weights(double eps, double (&w)[P + 1]) {
+    constexpr int L = Stencil<P>::L, R = Stencil<P>::R;
+    const double z = -eps;
+#pragma unroll
+    for (int col = 0; col <= P; ++col) {
+        const int j = col - L;
+        double num = 1.0;
+#pragma unroll
+        for (int q = -L; q <= R; ++q)
+            if (q != j) num = __dmul_rn(num, __dsub_rn(z, (double)q));
+        const double den = lagrange_den<P>(col);
+        w[col] = div_const(num, den, 1.0 / den);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// truncation-error polynomial f(z) = prod_{q=-l}^{r}(q + z) / (p+1)!
+// (coarse_correction.py:22-32) — setup only, true division.
+template <int P>
+__device__ __forceinline__ double f_poly(double z) {
+    constexpr int L = Stencil<P>::L, R = Stencil<P>::R;
+    double out = 1.0;
+#pragma unroll
+    for (int q = -L; q <= R; ++q) out = __dmul_rn(out, __dadd_rn((double)q, z));
+    double fact = 1.0;
+#pragma unroll
+    for (int k = 2; k <= P + 1; ++k) fact *= (double)k;
+    return __ddiv_rn(out, fact);
+}
+
+// D_{p+1} stencil coefficients (coarse_correction.py:35-47)
+template <int P>
+__device__ __forceinline__ double dcoef(int idx);
+template <>
+__device__ __forceinline__ double dcoef<1>(int i) {
+    const double c[3] = {1.0, -2.0, 1.0};
+    return c[i];
+}
+template <>
+__device__ __forceinline__ double dcoef<3>(int i) {
+    const double c[5] = {1.0, -4.0, 6.0, -4.0, 1.0};
+    return c[i];
+}
+template <>
+__device__ __forceinline__ double dcoef<5>(int i) {
+    const double c[7] = {1.0, -6.0, 15.0, -20.0, 15.0, -6.0, 1.0};
+    return c[i];
+}
+
+// ---------------------------------------------------------------------------
+// deterministic reductions
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;  // identical in every lane (commutative butterfly)
+}
+
+// Block-wide sum; `red` needs NT/32 + 1 doubles of shared memory.  Fixed
+// order: per-warp butterfly, then warp 0 sums the warp partials.  Ends with a
+// barrier so `red` can be reused immediately.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double t = lane < NW ? red[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) red[NW] = t;
+    }
+    __syncthreads();
+    double r = red[NW];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// wave speeds (core.py:130-153 + BASELINE B2/B4).  Expression order follows
+// oracle/mgrit_oracle.py:SPEEDS; only sin/cos differ from numpy (<= ulps).
+
+constexpr double kPi = 3.141592653589793;
+constexpr double kTwoPi = 2.0 * kPi;  // == Python 2.0 * np.pi (exact doubling)
+
+__device__ __forceinline__ void wave_speed(int id, double x, double y, double t,
+                                           double &ax, double &ay) {
+    switch (id) {
+        case MGRIT_SPEED_C1: ax = 1.0; ay = 0.0; break;
+        case MGRIT_SPEED_C2: ax = __dmul_rn(cos(__dmul_rn(kTwoPi, t)), 1.0); ay = 0.0; break;
+        case MGRIT_SPEED_C3:
+            ax = __dmul_rn(cos(__dmul_rn(kTwoPi, t)), cos(__dmul_rn(kTwoPi, x)));
+            ay = 0.0;
+            break;
+        case MGRIT_SPEED_C4: ax = 1.0; ay = 1.0; break;
+        case MGRIT_SPEED_C5: {
+            double ct = cos(__ddiv_rn(__dmul_rn(kTwoPi, t), 3.4));
+            double sy = sin(__dmul_rn(kPi, y));
+            double cx = cos(__dmul_rn(kPi, x));
+            ax = __dmul_rn(__dmul_rn(sy, sy), ct);
+            ay = __dmul_rn(-__dmul_rn(cx, cx), ct);
+            break;
+        }
+        case MGRIT_SPEED_B2:
+            ax = __dadd_rn(1.0, __dmul_rn(__dmul_rn(0.5, sin(__dmul_rn(kTwoPi, x))),
+                                         cos(__dmul_rn(kTwoPi, t))));
+            ay = 0.0;
+            break;
+        case MGRIT_SPEED_B4: {
+            double ct = cos(__dmul_rn(kTwoPi, t));
+            double cx = cos(__dmul_rn(kPi, x));
+            double sy = sin(__dmul_rn(kPi, y));
+            ax = __dadd_rn(__dmul_rn(__dmul_rn(cx, cx), ct), 0.5);
+            ay = __dadd_rn(__dmul_rn(__dmul_rn(sy, sy), ct), 0.5);
+            break;
+        }
+        default: ax = 0.0; ay = 0.0; break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// error plumbing
+
+void set_error(const char *what, cudaError_t e);
+int check_launch(const char *what);
+
+}  // namespace mgrit

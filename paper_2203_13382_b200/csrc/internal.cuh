@@ -1,0 +1,28 @@
+// internal.cuh — declarations shared between the kernel families and capi.cu.
+#pragma once
+#include "common.cuh"
+
+namespace mgrit {
+
+struct RowsArgs {
+    int64_t B;
+    const int64_t *t_idx;
+    int64_t t_first, t_stride;
+    const double *U_in; int64_t ld_in;
+    const double *G; int64_t ld_g;
+    const double *U_sub; int64_t ld_sub;
+    double *out; int64_t ld_out;
+    double *row_sumsq;
+    int32_t *gmres_iters;
+};
+
+int apply_rows_1d(const mgrit_level_desc *L, const RowsArgs &a, void *scratch,
+                  int64_t scratch_bytes, int32_t *status, cudaStream_t st);
+int level_phase_1d(const mgrit_level_desc *L, const mgrit_phase_args *A, void *scratch,
+                   int64_t scratch_bytes, int32_t *status, cudaStream_t st);
+int sweep_1d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg,
+             int zero_init, int32_t *gmres_iters, void *scratch, int64_t scratch_bytes,
+             int32_t *status, cudaStream_t st);
+int64_t rows_capacity(const mgrit_level_desc *L);
+
+}  // namespace mgrit

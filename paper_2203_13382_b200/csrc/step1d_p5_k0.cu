@@ -1,0 +1,4 @@
+// step1d_p5_k0.cu — instantiation unit: 1D kernels for p=5, kind=MGRIT_KIND_SL.
+#define MGRIT_LAUNCH1D_IMPL
+#include "step1d_kernels.cuh"
+template struct mgrit::Launch1D<5, MGRIT_KIND_SL>;

@@ -1,0 +1,743 @@
+"""MGRIT driver and Level operator API on B200 (mirror of mgrit.py:1-390).
+
+Same names, signatures and in-place semantics as the reference's public API
+(``SolverConfig``, ``Level.step/step_batch``, ``build_hierarchy``,
+``f_relax``, ``c_relax``, ``residual``, ``solve_sequential``, ``v_cycle``,
+``solve``, ``sequential_reference``), but every operator application runs in
+hand-written sm_100a kernels (libmgrit_b200.so) on HBM-resident state.
+
+``solve`` uses the fused level engine (``_FusedCycle``): per level and cycle
+three kernels — F+C relaxation, F-relaxation + C-point residual/restriction,
+injection + post F-relaxation (+ the fine residual for the convergence test)
+— captured into one CUDA graph.  The reference-structured ``v_cycle`` (one
+launch per batched step, exactly mgrit.py:317-334) remains available and is
+what the drop-in functions compose; both paths give identical iterates.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field, replace
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import (Grid1D, Grid2D, WaveSpeed, get_wave_speed, initial_condition, pcg64_uniform,
+                   require_cuda, stream_ptr, device_sum)
+
+OPERATOR_KINDS = ("rediscretized", "corrected", "ideal", "forward_euler")
+DEPARTURE_POLICIES = ("backtrack", "erk_rediscretized", "erk_substeps")
+DEFAULT_CFL = 0.85
+_KIND_CODE = {"fine": _lib.KIND_SL, "rediscretized": _lib.KIND_SL, "corrected": _lib.KIND_CORRECTED,
+              "forward_euler": _lib.KIND_FORWARD_EULER}
+
+
+@dataclass(frozen=True)
+class GmresConfig:
+    """coarse_correction.py:157-170 — tol None runs exactly max_iters iterations."""
+
+    max_iters: int = 10
+    tol: float | None = None
+
+    def __post_init__(self):
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be at least 1")
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """mgrit.py:39-86, plus BASELINE hooks ``u0`` ("reference" | "sin4") and
+    ``iterate`` ("uniform01" = reference, "pm1" = uniform [-1, 1))."""
+
+    n_x: int
+    n_t: int
+    dim: int = 1
+    wave_speed: str | WaveSpeed = "C1"
+    p: int = 1
+    r: int | None = None
+    dt: float | None = None
+    schedule: int | Sequence[int] = 4
+    max_levels: int | None = None
+    operator_kind: str = "corrected"
+    departure_policy: str = "backtrack"
+    gmres_mode: str | None = None
+    relaxation: str = "FCF"
+    seed: int = 0
+    rtol: float = 1e-10
+    max_iters: int = 100
+    divergence_factor: float = 1e6
+    u0: str = "reference"
+    iterate: str = "uniform01"
+
+    def __post_init__(self):
+        if self.p % 2 == 0:
+            raise ValueError("interpolation degree p must be odd")
+        if self.p not in (1, 3, 5):
+            raise ValueError(f"unsupported interpolation degree p={self.p}; supported: (1, 3, 5)")
+        if self.operator_kind not in OPERATOR_KINDS:
+            raise ValueError(f"unknown operator kind {self.operator_kind!r}")
+        if self.departure_policy not in DEPARTURE_POLICIES:
+            raise ValueError(f"unknown departure policy {self.departure_policy!r}")
+        if self.relaxation not in ("FCF", "F"):
+            raise ValueError("relaxation must be 'FCF' or 'F'")
+        if self.gmres_mode not in (None, "fixed", "tolerance"):
+            raise ValueError("gmres_mode must be 'fixed', 'tolerance', or None")
+        if self.u0 not in ("reference", "sin4"):
+            raise ValueError("u0 must be 'reference' or 'sin4'")
+        if self.iterate not in ("uniform01", "pm1"):
+            raise ValueError("iterate must be 'uniform01' or 'pm1'")
+        speed = self.speed
+        if speed.dim != self.dim:
+            raise ValueError(f"wave speed {speed.name} is {speed.dim}D but config is {self.dim}D")
+
+    @property
+    def speed(self) -> WaveSpeed:
+        return get_wave_speed(self.wave_speed) if isinstance(self.wave_speed, str) else self.wave_speed
+
+    @property
+    def erk_order(self) -> int:
+        return self.p if self.r is None else self.r
+
+    def schedule_factor(self, level_index: int) -> int:
+        if isinstance(self.schedule, int):
+            return self.schedule
+        seq = list(self.schedule)
+        return seq[min(level_index, len(seq) - 1)]
+
+
+# ---------------------------------------------------------------------------
+# device workspace shared by the operator calls
+
+
+class _Workspace:
+    def __init__(self):
+        self.scratch: torch.Tensor | None = None
+        self.status: torch.Tensor | None = None
+
+    def get_scratch(self, nbytes: int, device) -> torch.Tensor:
+        if nbytes <= 0:
+            return None
+        if self.scratch is None or self.scratch.numel() < nbytes or self.scratch.device != device:
+            self.scratch = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
+        return self.scratch
+
+    def get_status(self, device) -> torch.Tensor:
+        if self.status is None or self.status.device != device:
+            self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        return self.status
+
+
+_WS = _Workspace()
+
+
+def _ptr(t):
+    return 0 if t is None else t.data_ptr()
+
+
+def _check_status(device):
+    st = _WS.get_status(device)
+    if int(st.item()) != 0:
+        st.zero_()
+        raise ValueError("non-finite right-hand side in gmres_solve")
+
+
+# ---------------------------------------------------------------------------
+# Level
+
+
+@dataclass
+class Level:
+    """One level of the hierarchy (mgrit.py:89-167) with device-resident records.
+
+    ``s_x``/``s_y``: departure records [S, n_points] as the scaled periodic
+    coordinate s = mod(x_dep - x_lo, L)/h (east index and eps re-derived
+    exactly on every application); ``disp_x``/``disp_y``: displacements kept
+    while coarser levels are built; ``sig_x``/``sig_y``: sigma fields.
+    """
+
+    index: int
+    grid: Grid1D | Grid2D
+    p: int
+    n_steps: int
+    dt: float
+    kind: str
+    s_x: torch.Tensor | None = None
+    s_y: torch.Tensor | None = None
+    disp_x: torch.Tensor | None = field(default=None, repr=False)
+    disp_y: torch.Tensor | None = field(default=None, repr=False)
+    sig_x: torch.Tensor | None = field(default=None, repr=False)
+    sig_y: torch.Tensor | None = field(default=None, repr=False)
+    gmres_cfg: GmresConfig | None = None
+    cf: int | None = None
+    finer: "Level | None" = None
+    shared: bool = False
+    stencil_numba: bool = False
+
+    @property
+    def sigma(self):
+        return None if self.sig_x is None else (self.sig_x, self.sig_y)
+
+    def desc(self, stencil_numba: bool | None = None) -> _lib.LevelDesc:
+        if self.kind == "ideal":
+            raise ValueError("the ideal operator is composed from the finer level")
+        d = _lib.LevelDesc()
+        d.dim = self.grid.dim
+        d.n_x = self.grid.n_x
+        d.p = self.p
+        d.kind = _KIND_CODE[self.kind]
+        d.shared = int(self.shared)
+        d.n_steps = self.n_steps
+        d.n_points = self.grid.n_points
+        d.s_x = _ptr(self.s_x)
+        d.s_y = _ptr(self.s_y)
+        d.sig_x = _ptr(self.sig_x)
+        d.sig_y = _ptr(self.sig_y)
+        g = self.gmres_cfg or GmresConfig()
+        d.gmres_max_iters = g.max_iters
+        d.gmres_tol = -1.0 if g.tol is None else float(g.tol)
+        d.stencil_numba = int(self.stencil_numba if stencil_numba is None else stencil_numba)
+        return d
+
+    @property
+    def device(self):
+        return self.s_x.device if self.s_x is not None else self.finer.device
+
+    # -- operator application (mgrit.py:135-167) ----------------------------
+
+    def _apply(self, U_in: torch.Tensor, t_first: int, t_stride: int, B: int, out: torch.Tensor,
+               G: torch.Tensor | None = None, U_sub: torch.Tensor | None = None,
+               t_idx: torch.Tensor | None = None, row_sumsq: torch.Tensor | None = None,
+               ld_in: int | None = None, ld_out: int | None = None, ld_g: int | None = None,
+               ld_sub: int | None = None, gmres_iters: torch.Tensor | None = None):
+        """Thin wrapper of mgrit_apply_rows (row pointers/strides in elements)."""
+        lib = _lib.load()
+        n = self.grid.n_points
+        d = self.desc()
+        dev = U_in.device
+        rows = min(B, max(1, int(lib.mgrit_resident_rows(ctypes.byref(d))) or B))
+        nbytes = int(lib.mgrit_gmres_scratch_bytes(ctypes.byref(d), rows))
+        scr = _WS.get_scratch(nbytes, dev)
+        rc = lib.mgrit_apply_rows(
+            ctypes.byref(d), B, _ptr(t_idx), t_first, t_stride,
+            U_in.data_ptr(), ld_in or n, _ptr(G), ld_g or n, _ptr(U_sub), ld_sub or n,
+            out.data_ptr(), ld_out or n, _ptr(row_sumsq), _ptr(gmres_iters), _ptr(scr),
+            0 if scr is None else scr.numel(), _WS.get_status(dev).data_ptr(), stream_ptr())
+        _lib.check(rc, "apply_rows")
+
+    def step(self, n: int, u: torch.Tensor) -> torch.Tensor:
+        """Advance u across step n (operator only, no forcing)."""
+        u = _as_device_vec(u, self)
+        if self.kind == "ideal":
+            ratio = self.finer.n_steps // self.n_steps
+            for k in range(ratio):
+                u = self.finer.step(n * ratio + k, u)
+            return u
+        out = torch.empty_like(u)
+        self._apply(u.reshape(1, -1), int(n), 0, 1, out.reshape(1, -1))
+        if self.kind == "corrected":
+            _check_status(u.device)
+        return out
+
+    def step_batch(self, t_idx, U: torch.Tensor) -> torch.Tensor:
+        """Apply the steps t_idx to the matching rows of U (returns a new tensor)."""
+        U = _as_device_mat(U, self)
+        t = torch.as_tensor(np.asarray(t_idx, dtype=np.int64)).to(U.device)
+        if self.kind == "ideal":
+            ratio = self.finer.n_steps // self.n_steps
+            V = U
+            for k in range(ratio):
+                V = self.finer.step_batch((t * ratio + k).cpu().numpy(), V)
+            return V if V is not U else U.clone()
+        out = torch.empty_like(U)
+        if U.shape[0]:
+            self._apply(U, 0, 0, U.shape[0], out, t_idx=t)
+            if self.kind == "corrected":
+                _check_status(U.device)
+        return out
+
+
+def _as_device_vec(u, lev) -> torch.Tensor:
+    if isinstance(u, np.ndarray):
+        u = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)).to(lev.device)
+    if u.shape[-1] != lev.grid.n_points:
+        raise ValueError(f"state length {u.shape[-1]} does not match grid size {lev.grid.n_points}")
+    return u.contiguous()
+
+
+def _as_device_mat(U, lev) -> torch.Tensor:
+    if isinstance(U, np.ndarray):
+        U = torch.from_numpy(np.ascontiguousarray(U, dtype=np.float64)).to(lev.device)
+    if U.shape[-1] != lev.grid.n_points:
+        raise ValueError(f"state length {U.shape[-1]} does not match grid size {lev.grid.n_points}")
+    return U.contiguous()
+
+
+@dataclass
+class ConvergenceReport:
+    """mgrit.py:170-178 (+ per-phase device timings)."""
+
+    residual_norms: np.ndarray
+    iterations: int
+    status: str
+    final_factor: float
+    wall_time: float = 0.0
+    setup_time: float = 0.0
+    solve_time: float = 0.0
+
+
+# ---------------------------------------------------------------------------
+# hierarchy construction on the device (mgrit.py:185-269, K1-K3)
+
+
+def _alloc_records(S, n, dim, dev):
+    s_x = torch.empty((S, n), dtype=torch.float64, device=dev)
+    d_x = torch.empty_like(s_x)
+    s_y = torch.empty_like(s_x) if dim == 2 else None
+    d_y = torch.empty_like(s_x) if dim == 2 else None
+    return s_x, s_y, d_x, d_y
+
+
+def _erk(grid, speed: WaveSpeed, order, S, dt, n_sub, dt_sub, dev):
+    if speed.device is None:
+        raise ValueError(f"wave speed {speed.name!r} has no device form; pass fine_coords= to build_hierarchy")
+    s_x, s_y, d_x, d_y = _alloc_records(S, grid.n_points, grid.dim, dev)
+    tab = _lib.erk_tableau(order)
+    rc = _lib.load().mgrit_erk_departures(grid.dim, grid.n_x, _lib.SPEED_IDS[speed.device], ctypes.byref(tab),
+                                          0, S, float(dt), int(n_sub), float(dt_sub), s_x.data_ptr(),
+                                          _ptr(s_y), d_x.data_ptr(), _ptr(d_y), stream_ptr())
+    _lib.check(rc, "erk_departures")
+    return s_x, s_y, d_x, d_y
+
+
+def departures_from_coords(grid, coords, dev=None):
+    """Records from caller-traced departure coordinates, shape (S, n) per axis
+    (DepartureSet*.from_coords, semi_lagrangian.py:175-205)."""
+    dev = dev or require_cuda()
+    cs = [coords] if grid.dim == 1 else list(coords)
+    cs = [torch.as_tensor(np.asarray(c, dtype=np.float64)).reshape(-1, grid.n_points).to(dev) for c in cs]
+    S = cs[0].shape[0]
+    s_x, s_y, d_x, d_y = _alloc_records(S, grid.n_points, grid.dim, dev)
+    rc = _lib.load().mgrit_departures_from_coords(grid.dim, grid.n_x, S, cs[0].data_ptr(),
+                                                  _ptr(cs[1] if grid.dim == 2 else None), s_x.data_ptr(),
+                                                  _ptr(s_y), d_x.data_ptr(), _ptr(d_y), stream_ptr())
+    _lib.check(rc, "departures_from_coords")
+    return s_x, s_y, d_x, d_y
+
+
+def build_hierarchy(cfg: SolverConfig, fine_coords=None, keep_displacements: bool = False) -> list[Level]:
+    """Build the level hierarchy on the device (mgrit.py:217-269).
+
+    Fine departures come from the device ERK tracer (or ``fine_coords``,
+    caller-traced departure coordinates of shape (S, n_points) per axis);
+    coarse departures follow ``cfg.departure_policy``; sigma fields follow
+    phi_field/sigma_accumulate.  Displacements are dropped once the next
+    coarser level exists unless ``keep_displacements``.
+    """
+    dev = require_cuda()
+    speed = cfg.speed
+    if speed.dim != cfg.dim:
+        raise ValueError(f"wave speed {speed.name} is {speed.dim}D but config is {cfg.dim}D")
+    grid = Grid1D(cfg.n_x) if cfg.dim == 1 else Grid2D(cfg.n_x)
+    dt = cfg.dt if cfg.dt is not None else DEFAULT_CFL * grid.h
+    order = cfg.erk_order
+    lib = _lib.load()
+    shared = speed.constant
+    S0 = 1 if shared else cfg.n_t
+    if fine_coords is not None:
+        rec = departures_from_coords(grid, fine_coords, dev)
+        if rec[0].shape[0] != S0:
+            raise ValueError(f"fine_coords must hold {S0} departure sets")
+    else:
+        rec = _erk(grid, speed, order, S0, dt, 1, dt, dev)
+    fine = Level(0, grid, cfg.p, cfg.n_t, dt, "fine", rec[0], rec[1], rec[2], rec[3], shared=shared)
+    levels = [fine]
+    while True:
+        if cfg.max_levels is not None and len(levels) >= cfg.max_levels:
+            break
+        prev = levels[-1]
+        m = cfg.schedule_factor(len(levels) - 1)
+        if prev.n_steps % m != 0 or prev.n_steps // m < 2:
+            break
+        n_c = prev.n_steps // m
+        dt_c = prev.dt * m
+        kind = cfg.operator_kind
+        if kind == "ideal":
+            lvl = Level(len(levels), grid, cfg.p, n_c, dt_c, "ideal", finer=prev)
+        else:
+            S = 1 if shared else n_c
+            if cfg.departure_policy == "backtrack":
+                s_x, s_y, d_x, d_y = _alloc_records(S, grid.n_points, grid.dim, dev)
+                rc = lib.mgrit_backtrack(grid.dim, grid.n_x, m, S, int(prev.shared), prev.disp_x.data_ptr(),
+                                         _ptr(prev.disp_y), s_x.data_ptr(), _ptr(s_y), d_x.data_ptr(),
+                                         _ptr(d_y), stream_ptr())
+                _lib.check(rc, "backtrack")
+            elif cfg.departure_policy == "erk_rediscretized":
+                s_x, s_y, d_x, d_y = _erk(grid, speed, order, S, dt_c, 1, dt_c, dev)
+            else:
+                n_sub = int(round(dt_c / dt))
+                s_x, s_y, d_x, d_y = _erk(grid, speed, order, S, dt_c, n_sub, dt, dev)
+            sig_x = sig_y = None
+            if kind in ("corrected", "forward_euler"):
+                sig_x = torch.empty((S, grid.n_points), dtype=torch.float64, device=dev)
+                sig_y = torch.empty_like(sig_x) if grid.dim == 2 else None
+                rc = lib.mgrit_phi_sigma(grid.dim, grid.n_x, cfg.p, m, S, int(prev.shared), s_x.data_ptr(),
+                                         _ptr(s_y), prev.s_x.data_ptr(), _ptr(prev.s_y), _ptr(prev.sig_x),
+                                         _ptr(prev.sig_y), sig_x.data_ptr(), _ptr(sig_y), stream_ptr())
+                _lib.check(rc, "phi_sigma")
+            lvl = Level(len(levels), grid, cfg.p, n_c, dt_c, kind, s_x, s_y, d_x, d_y, sig_x, sig_y,
+                        finer=prev, shared=shared)
+        prev.cf = m
+        if not keep_displacements:
+            prev.disp_x = prev.disp_y = None
+        levels.append(lvl)
+    if len(levels) < 2:
+        raise ValueError("time grid does not admit any coarsening with the given schedule")
+    if not keep_displacements:
+        levels[-1].disp_x = levels[-1].disp_y = None
+    mode = cfg.gmres_mode or ("fixed" if len(levels) == 2 else "tolerance")
+    gcfg = GmresConfig(10, None) if mode == "fixed" else GmresConfig(10, 1e-2)
+    for lvl in levels[1:]:
+        lvl.gmres_cfg = gcfg
+    # the reference's numba sweep (mgrit.py:304-305) groups the D-stencil sum
+    # differently from the numpy operator; mirror it on 1D corrected levels with >= 64 steps
+    last = levels[-1]
+    last.stencil_numba = (last.grid.dim == 1 and last.kind == "corrected" and last.n_steps >= 64)
+    return levels
+
+
+# ---------------------------------------------------------------------------
+# relaxation, residual, cycling — reference-structured (mgrit.py:276-334)
+
+
+def _rows(U: torch.Tensor, start: int, step: int, count: int):
+    return U[start: start + step * (count - 1) + 1: step] if count > 0 else U[start:start]
+
+
+def f_relax(level: Level, U, G, m: int | None = None) -> None:
+    """mgrit.py:276-283 (in place; one batched launch per F-point offset)."""
+    U, G, wb = _io(level, U, G)
+    m = level.cf if m is None else m
+    N = level.n_steps
+    n_starts = (N + m - 1) // m
+    for k in range(1, m):
+        B = n_starts
+        if (n_starts - 1) * m + k > N:
+            raise IndexError(f"f_relax: step index {(n_starts - 1) * m + k} out of bounds for {N} steps")
+        _step_rows_strided(level, U, G, k - 1, m, B)
+    wb()
+
+
+def c_relax(level: Level, U, G, m: int | None = None) -> None:
+    """mgrit.py:286-290."""
+    U, G, wb = _io(level, U, G)
+    m = level.cf if m is None else m
+    B = level.n_steps // m
+    _step_rows_strided(level, U, G, m - 1, m, B)
+    wb()
+
+
+def _step_rows_strided(level, U, G, first, stride, B):
+    """U[first + b*stride + 1] = Phi U[first + b*stride] + G[...] for b < B."""
+    if B <= 0:
+        return
+    n = level.grid.n_points
+    if level.kind == "ideal":
+        t = np.arange(B) * stride + first
+        V = level.step_batch(t, U[first: first + stride * (B - 1) + 1: stride])
+        U[first + 1: first + 1 + stride * (B - 1) + 1: stride] = V + G[first + 1: first + 1 + stride * (B - 1) + 1: stride]
+        return
+    level._apply(U[first:], first, stride, B, U[first + 1:], G=G[first + 1:], ld_in=stride * n,
+                 ld_out=stride * n, ld_g=stride * n)
+    if level.kind == "corrected":
+        _check_status(U.device)
+
+
+def residual(level: Level, U, G):
+    """r_n = g_n + Phi u_{n-1} - u_n, r_0 = 0 (mgrit.py:293-299); new tensor."""
+    host = isinstance(U, np.ndarray)
+    U, G, _ = _io(level, U, G)
+    R = torch.empty_like(U)
+    R[0] = 0.0
+    N = level.n_steps
+    if level.kind == "ideal":
+        R[1:] = (G[1:] + level.step_batch(np.arange(N), U[:-1])) - U[1:]
+    else:
+        level._apply(U, 0, 1, N, R[1:], G=G[1:], U_sub=U[1:])
+        if level.kind == "corrected":
+            _check_status(U.device)
+    return R.cpu().numpy() if host else R
+
+
+def solve_sequential(level: Level, U, G) -> None:
+    """Exact sequential solve of a level (mgrit.py:302-314; numba sweep grouping
+    for 1D corrected levels with >= 64 steps)."""
+    U, G, wb = _io(level, U, G)
+    if level.kind == "ideal":
+        for n in range(1, level.n_steps + 1):
+            U[n] = level.step(n - 1, U[n - 1]) + G[n]
+        wb()
+        return
+    _sweep(level, U, G, zero_init=False)
+    wb()
+
+
+def _sweep(level: Level, U: torch.Tensor, G: torch.Tensor | None, zero_init: bool, numba=None):
+    lib = _lib.load()
+    numba = (level.grid.dim == 1 and level.kind == "corrected" and level.n_steps >= 64) if numba is None else numba
+    d = level.desc(stencil_numba=numba)
+    nbytes = int(lib.mgrit_gmres_scratch_bytes(ctypes.byref(d), 1))
+    scr = _WS.get_scratch(nbytes, U.device)
+    n = level.grid.n_points
+    rc = lib.mgrit_sequential_sweep(ctypes.byref(d), U.data_ptr(), n, _ptr(G), n, int(zero_init), 0, _ptr(scr),
+                                    0 if scr is None else scr.numel(), _WS.get_status(U.device).data_ptr(),
+                                    stream_ptr())
+    _lib.check(rc, "sequential_sweep")
+
+
+def _io(level, U, G):
+    """Accept numpy (copied to the device and written back) or device tensors."""
+    if isinstance(U, np.ndarray):
+        dev = level.device
+        Ud = torch.from_numpy(np.ascontiguousarray(U)).to(dev)
+        Gd = torch.from_numpy(np.ascontiguousarray(G)).to(dev)
+
+        def wb():
+            U[...] = Ud.cpu().numpy()
+        return Ud, Gd, wb
+    if not U.is_contiguous() or (G is not None and not G.is_contiguous()):
+        raise ValueError("U and G must be contiguous (n_rows, n_points) float64 tensors")
+    return U, G, (lambda: None)
+
+
+def v_cycle(levels: list[Level], li: int, U, G, relaxation: str = "FCF") -> None:
+    """One recursive V-cycle (mgrit.py:317-334), reference-structured."""
+    U, G, wb = _io(levels[li], U, G)
+    lev = levels[li]
+    if li == len(levels) - 1:
+        solve_sequential(lev, U, G)
+        wb()
+        return
+    m = lev.cf
+    f_relax(lev, U, G)
+    if relaxation == "FCF":
+        c_relax(lev, U, G)
+        f_relax(lev, U, G)
+    R = residual(lev, U, G)
+    Gc = R[::m].contiguous()
+    Uc = torch.zeros((lev.n_steps // m + 1, lev.grid.n_points), dtype=torch.float64, device=U.device)
+    v_cycle(levels, li + 1, Uc, Gc, relaxation)
+    U[::m] += Uc
+    f_relax(lev, U, G)
+    wb()
+
+
+# ---------------------------------------------------------------------------
+# fused engine
+
+
+class _FusedCycle:
+    """Device buffers + launch sequence of one V-cycle using the fused phase
+    kernels (1D, non-ideal levels)."""
+
+    def __init__(self, levels: list[Level], U: torch.Tensor, relaxation: str):
+        self.levels = levels
+        self.relaxation = relaxation
+        self.dev = U.device
+        n = levels[0].grid.n_points
+        L = len(levels)
+        self.U = [U] + [torch.zeros((lv.n_steps + 1, n), dtype=torch.float64, device=self.dev) for lv in levels[1:]]
+        self.G = [None] + [torch.zeros((lv.n_steps + 1, n), dtype=torch.float64, device=self.dev) for lv in levels[1:]]
+        self.C = [torch.zeros((lv.n_steps // lv.cf + 1, n), dtype=torch.float64, device=self.dev)
+                  for lv in levels[:-1]]
+        self.partial = torch.zeros(levels[0].n_steps // levels[0].cf, dtype=torch.float64, device=self.dev)
+        self.sumsq = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.status = _WS.get_status(self.dev)
+        lib = _lib.load()
+        self.descs = [lv.desc() for lv in levels[:-1]]
+        self.desc_last = levels[-1].desc(stencil_numba=levels[-1].stencil_numba)
+        need = 0
+        for lv, d in zip(levels[:-1], self.descs):
+            rows = min(lv.n_steps // lv.cf, max(1, int(lib.mgrit_resident_rows(ctypes.byref(d)))))
+            need = max(need, int(lib.mgrit_gmres_scratch_bytes(ctypes.byref(d), rows)))
+        need = max(need, int(lib.mgrit_gmres_scratch_bytes(ctypes.byref(self.desc_last), 1)))
+        self.scratch = torch.empty(max(need, 8), dtype=torch.uint8, device=self.dev)
+        self._args = {}
+        for li in range(L - 1):
+            for ph in (_lib.PHASE_FC, _lib.PHASE_F_RES, _lib.PHASE_FONLY_RES, _lib.PHASE_INJ_F):
+                self._args[(li, ph)] = self._make_args(li, ph)
+
+    def _make_args(self, li, phase):
+        lv = self.levels[li]
+        n = lv.grid.n_points
+        a = _lib.PhaseArgs()
+        a.phase = phase
+        a.m = lv.cf
+        a.c_begin = 0
+        a.c_count = lv.n_steps // lv.cf
+        a.n_intervals = lv.n_steps // lv.cf
+        a.U = self.U[li].data_ptr(); a.ldu = n; a.u_row0 = 0
+        a.G = _ptr(self.G[li]); a.ldg = n; a.g_row0 = 0
+        a.Cbuf = self.C[li].data_ptr()
+        a.Uc = self.U[li + 1].data_ptr()
+        a.Gc = self.G[li + 1].data_ptr() if phase in (_lib.PHASE_F_RES, _lib.PHASE_FONLY_RES) else 0
+        a.c_row0 = 0
+        a.partial = self.partial.data_ptr() if (li == 0 and phase == _lib.PHASE_INJ_F) else 0
+        a.partial0 = 0
+        a.zero_init = int(li > 0)
+        return a
+
+    def _phase(self, li, phase):
+        lib = _lib.load()
+        rc = lib.mgrit_level_phase(ctypes.byref(self.descs[li]), ctypes.byref(self._args[(li, phase)]),
+                                   self.scratch.data_ptr(), self.scratch.numel(), self.status.data_ptr(),
+                                   stream_ptr())
+        _lib.check(rc, "level_phase")
+
+    def cycle(self, li: int = 0):
+        if li == len(self.levels) - 1:
+            lib = _lib.load()
+            n = self.levels[li].grid.n_points
+            rc = lib.mgrit_sequential_sweep(ctypes.byref(self.desc_last), self.U[li].data_ptr(), n,
+                                            self.G[li].data_ptr(), n, 1, 0, self.scratch.data_ptr(),
+                                            self.scratch.numel(), self.status.data_ptr(), stream_ptr())
+            _lib.check(rc, "sequential_sweep")
+            return
+        if self.relaxation == "FCF":
+            self._phase(li, _lib.PHASE_FC)
+            self._phase(li, _lib.PHASE_F_RES)
+        else:
+            self._phase(li, _lib.PHASE_FONLY_RES)
+        self.cycle(li + 1)
+        self._phase(li, _lib.PHASE_INJ_F)
+
+    def iteration(self):
+        """One V-cycle + fine residual norm^2 into self.sumsq (device)."""
+        self.cycle(0)
+        _lib.check(_lib.load().mgrit_sum(self.partial.data_ptr(), self.partial.numel(), self.sumsq.data_ptr(),
+                                         stream_ptr()), "sum")
+
+
+def _fused_ok(levels):
+    return all(lv.kind != "ideal" and lv.grid.dim == 1 for lv in levels)
+
+
+def initial_state(cfg: SolverConfig, grid) -> np.ndarray:
+    return initial_condition(grid, cfg.u0)
+
+
+def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_iterate=None,
+          output: str = "numpy", use_graph: bool = True, engine: str = "auto"):
+    """Run MGRIT (mgrit.py:337-378) on the device.
+
+    ``initial_iterate``: optional host array (n_t, n_points) uploaded as U[1:];
+    by default U[1:] is numpy's ``default_rng(seed).random`` stream generated
+    bit-identically on the device (``iterate="pm1"`` maps it to [-1, 1)).
+    ``output``: "numpy" (reference behaviour, host copy of U) or "device".
+    ``engine``: "fused" (default when supported), "reference" (the
+    reference-structured v_cycle built from batched launches).
+    """
+    t_begin = time.perf_counter()
+    dev = require_cuda()
+    if levels is None:
+        levels = build_hierarchy(cfg)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_begin
+    t_solve0 = time.perf_counter()
+    fine = levels[0]
+    grid = fine.grid
+    n = grid.n_points
+    U = torch.empty((cfg.n_t + 1, n), dtype=torch.float64, device=dev)
+    U[0] = torch.from_numpy(initial_state(cfg, grid)).to(dev)
+    if initial_iterate is not None:
+        src = torch.as_tensor(initial_iterate)
+        U[1:].copy_(src.reshape(cfg.n_t, n), non_blocking=True)
+    else:
+        pcg64_uniform(cfg.seed, cfg.n_t, n, U[1:], pm1=(cfg.iterate == "pm1"))
+    status = _WS.get_status(dev)
+    status.zero_()
+    use_fused = (engine == "fused") or (engine == "auto" and _fused_ok(levels))
+    if use_fused and not _fused_ok(levels):
+        raise ValueError("fused engine supports 1D non-ideal hierarchies")
+
+    # initial residual r0 (all rows: the random iterate has F-point residuals)
+    row_ss = torch.empty(cfg.n_t, dtype=torch.float64, device=dev)
+    R = torch.empty((cfg.n_t, n), dtype=torch.float64, device=dev)
+    fine._apply(U, 0, 1, cfg.n_t, R, U_sub=U[1:], row_sumsq=row_ss)
+    r0 = float(torch.sqrt(device_sum(row_ss)).item())
+    del R
+    history = [r0]
+    state = "max_iters"
+    G0 = torch.zeros_like(U) if not use_fused else None
+
+    if use_fused:
+        eng = _FusedCycle(levels, U, cfg.relaxation)
+        graph = None
+        for it in range(cfg.max_iters):
+            if graph is not None:
+                graph.replay()
+            else:
+                eng.iteration()
+                if use_graph and it == 0 and cfg.max_iters > 1:
+                    graph = _capture(eng.iteration)
+            ss = float(eng.sumsq.item())
+            bad = int(status.item())
+            if bad:
+                history.append(float("nan"))
+                state = "diverged"
+                break
+            r = float(np.sqrt(ss))
+            history.append(r)
+            if not np.isfinite(r) or r >= cfg.divergence_factor * r0:
+                state = "diverged"
+                break
+            if r <= cfg.rtol * r0:
+                state = "converged"
+                break
+    else:
+        for _ in range(cfg.max_iters):
+            try:
+                v_cycle(levels, 0, U, G0, cfg.relaxation)
+                Rf = residual(fine, U, G0)
+                r = float(torch.sqrt(device_sum(torch.square(Rf).reshape(-1))).item())
+            except (ValueError, FloatingPointError):
+                history.append(float("nan"))
+                state = "diverged"
+                break
+            history.append(r)
+            if not np.isfinite(r) or r >= cfg.divergence_factor * r0:
+                state = "diverged"
+                break
+            if r <= cfg.rtol * r0:
+                state = "converged"
+                break
+    out = U.cpu().numpy() if output == "numpy" else U
+    torch.cuda.synchronize()
+    t_end = time.perf_counter()
+    hist = np.array(history)
+    factor = float(hist[-1] / hist[-2]) if len(hist) > 1 else float("nan")
+    rep = ConvergenceReport(hist, len(hist) - 1, state, factor, t_end - t_begin, t_setup, t_end - t_solve0)
+    return rep, out
+
+
+def _capture(fn):
+    """Capture ``fn``'s launches (all on the current stream) in a CUDA graph."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g
+
+
+def sequential_reference(cfg: SolverConfig, levels: list[Level] | None = None, output: str = "numpy"):
+    """Plain sequential time stepping of the fine level (mgrit.py:381-390) —
+    also the sequential GPU time-stepping baseline (one CTA walks all steps)."""
+    dev = require_cuda()
+    if levels is None:
+        levels = build_hierarchy(replace(cfg, max_levels=2))
+    fine = levels[0]
+    U = torch.empty((cfg.n_t + 1, fine.grid.n_points), dtype=torch.float64, device=dev)
+    U[0] = torch.from_numpy(initial_state(cfg, fine.grid)).to(dev)
+    _sweep(fine, U, None, zero_init=False)
+    return U.cpu().numpy() if output == "numpy" else U
