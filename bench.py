@@ -1,0 +1,455 @@
+"""Benchmark: MGRIT solve space-time DOF/s to 1e-10 relative residual.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
+
+One *step* = one complete MGRIT solve (BASELINE.json metric) of the chosen
+config from the prebuilt device hierarchy: U initialisation (numpy PCG64
+stream generated bit-identically on the device), initial residual, V-cycles
+and convergence residuals until ||r|| <= 1e-10 ||r0||.  Hierarchy setup
+(ERK tracing, backtracking, sigma) is excluded and reported separately, as in
+the reference's timing discussion.
+
+Default workload: BASELINE config 2 (configs[1]): 1D, n_x = n_t = 4096,
+a(x,t) = 1 + 0.5 sin(2 pi x) cos(2 pi t), p = 3, m = 4, FCF, multilevel
+(6 levels), seed 1, dt = 0.85 h (reference default).  U (134 MB) and the
+fine departure records (134 MB) exceed the 126 MB L2, so no explicit flush.
+
+``--impl reference`` times the reference's CPU implementation of the path —
+the oracle port under oracle/ (bit-identical to mgrit_advect; the reference
+is pure Python so there is nothing to compile into oracle/_ref) — on the
+host cores, one bounded sample (one V-cycle + convergence residual of the
+same config) per step, extrapolated to a full solve with the reference's own
+iteration count.
+
+N > 1 (torchrun): every rank solves its own replica of the config (the time
+axis is not yet sharded across ranks) — "scaling": "weak".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(n_x=1024, n_t=1024, wave_speed="C1", p=1, schedule=8, max_levels=2, dt=2.0 / 1024, seed=0,
+                 iterate="pm1"),
+    "cfg1_085h": dict(n_x=1024, n_t=1024, wave_speed="C1", p=1, schedule=8, max_levels=2, seed=0, iterate="pm1"),
+    "cfg2": dict(n_x=4096, n_t=4096, wave_speed="B2", p=3, schedule=4, seed=1),
+    "cfg3": dict(n_x=16384, n_t=16384, wave_speed="B2", p=5, schedule=8, seed=2),
+}
+DESCR = {
+    "cfg1": "BASELINE cfg1: 1D a=1, 1024x1024, p=1, two-level m=8, dt=2/nt (CFL 1), iterate U[-1,1) seed 0",
+    "cfg1_085h": "BASELINE cfg1 mesh at dt=0.85h (non-degenerate companion)",
+    "cfg2": "BASELINE cfg2: 1D a=1+0.5sin(2pi x)cos(2pi t), 4096x4096, p=3, m=4 multilevel FCF, seed 1, dt=0.85h",
+    "cfg3": "BASELINE cfg3: 1D same speed, 16384x16384, p=5, m=8 multilevel FCF, seed 2, dt=0.85h",
+}
+GOLDEN = {"cfg1": "cfg1_full", "cfg1_085h": "cfg1_085h", "cfg2": "cfg2_full"}
+
+
+def _golden(name):
+    g = GOLDEN.get(name)
+    if g is None:
+        return None
+    with open(os.path.join(ROOT, "tests", "golden", "index.json")) as f:
+        ix = json.load(f)
+    if g not in ix:
+        return None
+    hist = np.load(os.path.join(ROOT, "tests", "golden", f"solve_{g}.npz"))["hist"]
+    return ix[g], hist
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes of the fused phase kernels
+
+
+def phase_bytes(level, phase, fine: bool) -> int:
+    """Minimal HBM bytes one launch of a fused phase kernel must move.
+
+    8 B per node for every state row read/written, every departure record
+    (s) and sigma row read; GMRES Krylov traffic (on-chip/L2) is excluded."""
+    from paper_2203_13382_b200 import _lib
+    n = level.grid.n_points
+    N = level.n_steps
+    m = level.cf
+    nI = N // m
+    g = 0 if fine else 1           # G rows read (zero forcing on the fine level)
+    sig = 1 if level.kind != "fine" and level.sig_x is not None else 0
+    step = 8 * n * (1 + g + sig + 1)   # s + G + sigma + output row
+    if phase == _lib.PHASE_FC:
+        left = 0 if not fine else 8 * n
+        return nI * (left + m * step)
+    if phase == _lib.PHASE_F_RES:
+        per = 8 * n * 2 + (m - 1) * step + 8 * n * (1 + g + sig) + 8 * n * 3   # tail: s,G,sig + Cbuf r, U w, Gc w
+        return nI * per
+    if phase == _lib.PHASE_INJ_F:
+        per = 8 * n * 3 + (m - 1) * step + (8 * n * (1 + g + sig) + 16 * n if fine else 0)
+        return nI * per
+    return 0
+
+
+def run_gpu(args):
+    import torch
+    import paper_2203_13382_b200 as P
+    from paper_2203_13382_b200 import _lib
+    from paper_2203_13382_b200 import mgrit as M
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    kw = CONFIGS[args.config]
+    cfg = P.SolverConfig(**kw)
+    t0 = time.perf_counter()
+    levels = P.build_hierarchy(cfg)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    n_dof = cfg.n_x ** cfg.dim * cfg.n_t
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also compiles CUDA graphs / sets kernel attributes)
+    for _ in range(args.warmup):
+        rep, _ = P.solve(cfg, levels, output="device")
+    barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record()
+        for _ in range(args.steps):
+            rep, U = P.solve(cfg, levels, output="device")
+        stop.record()
+        barrier()
+    ms = start.elapsed_time(stop) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n_dof / (ms / 1e3)
+
+    # ---- end to end through the public API with host buffers
+    X = torch.from_numpy(np.random.default_rng(cfg.seed).random((cfg.n_t, cfg.n_x ** cfg.dim)))
+    if cfg.iterate == "pm1":
+        X = 2.0 * X - 1.0
+    Xp = X.pin_memory()
+    e2e_ms = []
+    for i in range(max(2, min(args.steps, 5))):
+        barrier()
+        t1 = time.perf_counter()
+        rep_e, Uh = P.solve(cfg, levels, initial_iterate=Xp, output="numpy")
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t1) * 1e3)
+    e2e = float(np.median(e2e_ms[1:]))
+    if dist is not None:
+        t = torch.tensor([e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    # ---- per-kernel breakdown of one V-cycle (eager launches, CUDA events)
+    breakdown, launches_iter = kernel_breakdown(levels, cfg)
+    top = max(breakdown, key=lambda k: breakdown[k]["ms_total"])
+    tb = breakdown[top]
+    peak = _peak()
+    achieved = tb["bytes"] / (tb["ms_avg"] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": peak["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / peak["hbm_gbs"], 4),
+                "traffic": _ncu_traffic(top), "bytes_per_launch": tb["bytes"],
+                "ms_per_launch": round(tb["ms_avg"], 5), "peak_source": peak["source"],
+                "share_of_iteration": round(tb["ms_total"] / sum(v["ms_total"] for v in breakdown.values()), 3)}
+
+    # ---- sequential GPU time stepping (fine level, one CTA walks all steps)
+    for _ in range(2):
+        P.sequential_reference(cfg, levels, output="device")
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(3):
+        P.sequential_reference(cfg, levels, output="device")
+    s1.record()
+    torch.cuda.synchronize()
+    seq_ms = s0.elapsed_time(s1) / 3
+
+    iters = rep.iterations
+    launches = 3 + 2 + launches_iter * iters      # pcg fill + r0 (rows + sum) + per-iteration
+    parity = None
+    gold = _golden(args.config)
+    if gold is not None:
+        info, hist = gold
+        dev_r0 = float(np.max(np.abs(rep.residual_norms - hist)) / hist[0]) if len(hist) == len(rep.residual_norms) else None
+        parity = {"iterations": iters, "reference_iterations": info["iterations"], "status": rep.status,
+                  "max_history_dev_over_r0": dev_r0}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.config, iters, args.cpu_samples)
+    if rank == 0:
+        line = {
+            "metric": "MGRIT solve space-time DOF/s to 1e-10 residual",
+            "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (BASELINE config; seeded PCG64 initial iterate)",
+            "config": {"workload": DESCR[args.config], "name": args.config, "n_x": cfg.n_x, "n_t": cfg.n_t,
+                       "p": cfg.p, "schedule": cfg.schedule, "levels": [lv.n_steps for lv in levels],
+                       "dt": levels[0].dt, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                       "l2": "inputs larger than L2 (U 134 MB + records 134 MB)",
+                       "setup_s": round(setup_s, 4), "iterations": iters, "status": rep.status},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": world * n_dof / (e2e / 1e3), "unit": "DOF/s", "ms_per_step": e2e,
+                    "h2d_bytes_per_step": int(X.numel() * 8 + cfg.n_x ** cfg.dim * 8),
+                    "d2h_bytes_per_step": int((cfg.n_t + 1) * cfg.n_x ** cfg.dim * 8)},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "sequential_gpu_ms": round(seq_ms, 3),
+            "speedup_vs_sequential_gpu": round(seq_ms / ms, 4),
+            "kernel_breakdown_ms": {k: round(v["ms_total"], 4) for k, v in breakdown.items()},
+            "parity": parity,
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def kernel_breakdown(levels, cfg, reps: int = 3):
+    """Time every launch of one V-cycle with CUDA events on the launching stream."""
+    import torch
+    from paper_2203_13382_b200 import _lib
+    from paper_2203_13382_b200 import mgrit as M
+    dev = torch.device("cuda")
+    U = torch.empty((cfg.n_t + 1, levels[0].grid.n_points), dtype=torch.float64, device=dev)
+    U[0] = 0.5
+    M.pcg64_uniform(cfg.seed, cfg.n_t, levels[0].grid.n_points, U[1:])
+    eng = M._FusedCycle(levels, U, cfg.relaxation)
+    names = {_lib.PHASE_FC: "FC", _lib.PHASE_F_RES: "F_RES", _lib.PHASE_FONLY_RES: "FONLY_RES",
+             _lib.PHASE_INJ_F: "INJ_F"}
+    rec = {}
+    orig_phase = eng._phase
+    stream = torch.cuda.current_stream()
+    count = [0]
+
+    def timed_phase(li, ph):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        orig_phase(li, ph)
+        b.record(stream)
+        key = f"L{li}_{names[ph]}_{levels[li].kind}"
+        rec.setdefault(key, []).append((a, b, phase_bytes(levels[li], ph, li == 0)))
+        count[0] += 1
+
+    eng._phase = timed_phase
+    orig_cycle = eng.cycle
+
+    def timed_cycle(li=0):
+        if li == len(levels) - 1:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            orig_cycle(li)
+            b.record(stream)
+            rec.setdefault(f"L{li}_sweep_{levels[li].kind}", []).append((a, b, 0))
+            count[0] += 1
+            return
+        _cycle_body(li)
+
+    def _cycle_body(li):
+        if eng.relaxation == "FCF":
+            eng._phase(li, _lib.PHASE_FC)
+            eng._phase(li, _lib.PHASE_F_RES)
+        else:
+            eng._phase(li, _lib.PHASE_FONLY_RES)
+        timed_cycle(li + 1)
+        eng._phase(li, _lib.PHASE_INJ_F)
+
+    for _ in range(reps):
+        count[0] = 0
+        timed_cycle(0)
+        torch.cuda.synchronize()
+    out = {}
+    for k, lst in rec.items():
+        ms = [a.elapsed_time(b) for a, b, _ in lst]
+        out[k] = {"ms_total": float(np.sum(ms)) / reps, "ms_avg": float(np.mean(ms)), "bytes": lst[0][2]}
+    return out, count[0] + 1   # + the norm sum
+
+
+def _peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def _ncu_traffic(kernel_key):
+    """DRAM bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(kernel_key)
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = the reference's algorithm, bit-identical)
+
+
+def _oracle_sample(name: str):
+    """One V-cycle + convergence residual of the config on the host (seconds),
+    plus the initial-residual time."""
+    import oracle as O
+    kw = CONFIGS[name]
+    ocfg = O.OConfig(**kw)
+    levels = O.hierarchy(ocfg)
+    fine = levels[0]
+    U = np.empty((ocfg.n_t + 1, fine.n_points))
+    U[0] = O.initial_state(ocfg)
+    U[1:] = O.initial_iterate(ocfg)
+    G = np.zeros_like(U)
+    t0 = time.perf_counter()
+    O.st_norm(O.residual(fine, U, G))
+    t_r0 = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    O.v_cycle(levels, 0, U, G, ocfg.relaxation)
+    O.st_norm(O.residual(fine, U, G))
+    t_it = time.perf_counter() - t1
+    return t_r0, t_it, levels
+
+
+def cpu_baseline(name: str, iters: int, samples: int = 1):
+    kw = CONFIGS[name]
+    n_dof = kw["n_x"] * kw["n_t"]
+    best = None
+    for _ in range(max(1, samples)):
+        t_r0, t_it, _ = _oracle_sample(name)
+        best = (t_r0, t_it) if best is None or t_it < best[1] else best
+    t_r0, t_it = best
+    est = t_r0 + iters * t_it
+    return {"value": n_dof / est, "unit": "DOF/s", "cores": 1, "kind": "port",
+            "sample": f"oracle (bit-identical numpy/C restatement of mgrit_advect): initial residual "
+                      f"({t_r0:.2f}s) + one V-cycle with convergence residual ({t_it:.2f}s) of {name}, "
+                      f"extrapolated x{iters} iterations; setup excluded",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    kw = CONFIGS[args.config]
+    gold = _golden(args.config)
+    iters = gold[0]["iterations"] if gold else 19
+    n_dof = kw["n_x"] * kw["n_t"]
+    times = []
+    for i in range(args.warmup + args.steps):
+        t_r0, t_it, _ = _oracle_sample(args.config)
+        if i >= args.warmup:
+            times.append(t_r0 + iters * t_it)
+    est = float(np.mean(times))
+    value = n_dof / est
+    line = {
+        "impl": "reference", "metric": "MGRIT solve space-time DOF/s to 1e-10 residual", "value": value,
+        "unit": "DOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": DESCR[args.config], "name": args.config},
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": "port",
+                         "sample": f"per step: oracle initial residual + one V-cycle + residual of {args.config}, "
+                                   f"extrapolated to the reference's {iters} iterations (setup excluded)",
+                         "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-samples", type=int, default=1)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -39,7 +39,7 @@ __all__ = [
     "f_poly", "d_stencil", "circulant", "imsd", "phi_sigma", "gmres",
     "backtrack", "OLevel", "OConfig", "hierarchy", "f_relax", "c_relax",
     "residual", "solve_sequential", "v_cycle", "solve", "sequential",
-    "initial_state", "initial_iterate", "st_norm", "sweep_available",
+    "initial_state", "initial_iterate", "st_norm", "sweep_available", "GmresLog", "OReport",
 ]
 
 TWO_PI = 2.0 * np.pi
@@ -695,7 +695,7 @@ class OReport:
     gmres_counts: list | None = None
 
 
-def solve(cfg: OConfig, levels=None, on_iter: Callable | None = None, log_gmres=False):
+def solve(cfg: OConfig, levels=None, on_iter: Callable | None = None, log_gmres=False, iterate0=None):
     """mgrit.py:337-378 with BASELINE's u0/iterate hooks and an optional
     per-iteration callback ``on_iter(k, U)`` for snapshots."""
     t0 = time.perf_counter()
@@ -707,7 +707,7 @@ def solve(cfg: OConfig, levels=None, on_iter: Callable | None = None, log_gmres=
     fine = levels[0]
     U = np.empty((cfg.n_t + 1, fine.n_points))
     U[0] = initial_state(cfg)
-    U[1:] = initial_iterate(cfg)
+    U[1:] = initial_iterate(cfg) if iterate0 is None else iterate0
     G = np.zeros_like(U)
     r0 = st_norm(residual(fine, U, G))
     hist = [r0]
