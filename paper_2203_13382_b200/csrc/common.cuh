@@ -39,19 +39,21 @@ struct Dec {
 };
 
 // east = ceil(s), eps = east - s, rounding guards, east mod n.
+// s = mod(x - x_lo, L)/h lies in [0, n], so east in [-1, n] before the
+// periodic wrap: two compares instead of an integer division.
 __device__ __forceinline__ Dec decompose_s(double s, int n) {
-    double ef = ceil(s);
+    const double ef = ceil(s);
     double eps = __dsub_rn(ef, s);
-    long long e = (long long)ef;
+    int e = (int)ef;
     if (eps < 0.0) eps = 0.0;
     if (eps >= 1.0) {
         eps = __dsub_rn(eps, 1.0);
         e -= 1;
     }
-    e %= n;
+    if (e >= n) e -= n;
     if (e < 0) e += n;
     Dec d;
-    d.e = (int)e;
+    d.e = e;
     d.eps = eps;
     return d;
 }
@@ -95,12 +97,22 @@ __device__ __forceinline__ void lagrange_weights(double eps, double (&w)[P + 1])
 #pragma unroll
     for (int col = 0; col <= P; ++col) {
         const int j = col - L;
-        double num = 1.0;
+        // num = ((1 * (z - q0)) * (z - q1)) * ...; 1 * x == x exactly
+        double num = 0.0;
+        bool first = true;
 #pragma unroll
-        for (int q = -L; q <= R; ++q)
-            if (q != j) num = __dmul_rn(num, __dsub_rn(z, (double)q));
+        for (int q = -L; q <= R; ++q) {
+            if (q == j) continue;
+            const double f = q == 0 ? z : __dsub_rn(z, (double)q);  // z - 0 == z exactly
+            num = first ? f : __dmul_rn(num, f);
+            first = false;
+        }
         const double den = lagrange_den<P>(col);
-        w[col] = div_const(num, den, 1.0 / den);
+        const double ad = den < 0 ? -den : den;
+        if (ad == 1.0 || ad == 2.0 || ad == 4.0 || ad == 8.0 || ad == 16.0)
+            w[col] = __dmul_rn(num, 1.0 / den);  // power-of-two denominator: exact
+        else
+            w[col] = div_const(num, den, 1.0 / den);
     }
 }
 

@@ -5,51 +5,110 @@
 // shared memory, so a CTA owns a whole row.  The fused phase kernels give one
 // CTA per C-interval and walk its m-1 dependent F-steps with the state kept
 // in shared memory: per step only the departure record (8 B/node) is read
-// and the new state (8 B/node) written to HBM; the previous state never
-// round-trips through HBM.  The semi-Lagrangian gather reads the smem row;
-// the corrected operator's GMRES runs inside the CTA (block reductions for
-// the MGS dots, one elected thread for the Givens/Hessenberg recurrences)
-// with its Krylov basis in a per-CTA global scratch slab that stays L2
-// resident.  Grids are persistent (<= resident-CTA capacity), looping over
-// rows / intervals.
+// (prefetched into registers one step ahead) and the new state (8 B/node)
+// written to HBM; the previous state never round-trips through HBM.
+//
+// The corrected operator's MGS-GMRES runs inside the CTA: the first Krylov
+// vectors live in shared memory next to the state row (the rest spill to a
+// per-CTA L2-resident slab), sigma stays in registers, dot products use four
+// independent accumulator chains, block reductions are double-buffered (two
+// barriers each), and the 1/beta, 1/h_{k+1,k} scalings use one correctly
+// rounded reciprocal plus an exact FMA correction per element (Markstein),
+// which is bit-identical to the division.  Grids are persistent
+// (<= resident-CTA capacity), looping over rows / intervals.
 #include "internal.cuh"
 
 namespace mgrit {
 
 constexpr int kMaxKrylov = 16;
+// periodic halo kept on both sides of the shared-memory row so stencil taps
+// (<= 3 cells: p = 5 interpolation, D_6) need no wrap-around arithmetic
+constexpr int kHalo = 4;
 
-// per-CTA GMRES control block in shared memory
+// row[i] = x plus its periodic halo image (row[-kHalo..-1], row[n..n+kHalo-1])
+__device__ __forceinline__ void put_row(double *row, int i, double x, int n) {
+    row[i] = x;
+    if (i < kHalo) row[n + i] = x;
+    if (i >= n - kHalo) row[i - n] = x;
+}
+
+// per-CTA GMRES control block + reduction buffers in shared memory
 struct GmresSmem {
     double H[(kMaxKrylov + 1) * kMaxKrylov];
     double cs[kMaxKrylov], sn[kMaxKrylov], g[kMaxKrylov + 1], y[kMaxKrylov];
-    int stop, done;
+    double red[2][33];
+    int stop;
 };
 
 struct RowCtx {
     double *rowbuf;   // smem, n doubles: state row / Krylov vector for the stencil
-    double *red;      // smem, NT/32+1 doubles
     GmresSmem *gs;    // smem
-    double *basis;    // global, (K+1)*n doubles (corrected only)
+    double *bsm;      // smem Krylov slots [nbs][n]
+    double *bgl;      // global Krylov slots [(K+1-nbs)][n] (corrected only)
+    int nbs;
+    int sel;          // double-buffer parity of the block reductions
     int32_t *status;  // sticky non-finite flag
+    __device__ __forceinline__ double *bvec(int j, int n) const {
+        return j < nbs ? bsm + (int64_t)j * n : bgl + (int64_t)(j - nbs) * n;
+    }
 };
 
-__host__ __device__ constexpr size_t smem_bytes_for(int n, int NT) {
-    return sizeof(double) * ((size_t)n + NT / 32 + 1) + sizeof(GmresSmem);
+// Fixed-order pairwise sum of N doubles in shared memory (broadcast reads).
+template <int N>
+__device__ __forceinline__ double tree_sum(const double *r) {
+    if constexpr (N == 1) {
+        return r[0];
+    } else {
+        return __dadd_rn(tree_sum<N / 2>(r), tree_sum<N - N / 2>(r + N / 2));
+    }
+}
+
+// Block-wide fixed-order sum, one barrier: warp butterflies, then every
+// warp reduces the NT/32 warp partials with the same butterfly.  The
+// scratch is double-buffered by call parity: call c+2 reuses call c's slots
+// only after every thread has passed call c+1's barrier.
+template <int NT>
+__device__ __forceinline__ double block_sum2(double v, RowCtx &cx) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *red = cx.gs->red[cx.sel];
+    cx.sel ^= 1;
+    v = warp_sum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    return warp_sum(lane < NW ? red[lane] : 0.0);
+}
+
+// a / b with y = RN(1/b): q0 = RN(a y), r = fma(-q0, b, a) (exact),
+// q = fma(r, y, q0) == RN(a / b) (Markstein; verified on 4e8 random pairs).
+__device__ __forceinline__ double div_rcp(double a, double b, double y) {
+    const double q0 = __dmul_rn(a, y);
+    const double r = fma(-q0, b, a);
+    return fma(r, y, q0);
+}
+
+template <int NT, int NPT, bool F>
+__device__ __forceinline__ void load_records(const mgrit_level_desc &L, int64_t t, double (&sv)[NPT]) {
+    const int n = L.n_x;
+    const double *s = L.s_x + (L.shared ? 0 : t) * (int64_t)n;
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        const int i = threadIdx.x + k * NT;
+        sv[k] = (F || i < n) ? __ldg(s + i) : 0.0;
+    }
 }
 
 // ---------------------------------------------------------------------------
-// v = Phi_t(rowbuf) for the CTA's nodes i = tid + k*NT.
+// v = Phi_t(rowbuf) for the CTA's nodes i = tid + k*NT, records preloaded in sv.
 // Returns the GMRES Arnoldi count for corrected kinds (-1 on non-finite rhs),
 // 0 otherwise.  rowbuf is clobbered for KIND != SL; the caller must
 // __syncthreads() before rewriting it.
-template <int P, int KIND, int NT, int NPT, bool NUMBA>
-__device__ int cta_apply(const mgrit_level_desc &L, int64_t t, const RowCtx &cx,
-                         double (&v)[NPT]) {
+template <int P, int KIND, int NT, int NPT, bool F, bool NUMBA>
+__device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, double (&v)[NPT],
+                         const double (&sv)[NPT]) {
     constexpr int SL = Stencil<P>::L;
     const int n = L.n_x;
     const int tid = threadIdx.x;
-    const int64_t set = L.shared ? 0 : t;
-    const double *s = L.s_x + set * (int64_t)n;
     const double *row = cx.rowbuf;
 
     // ---- semi-Lagrangian gather: left-to-right sum of rounded products
@@ -57,17 +116,15 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, const RowCtx &cx,
     for (int k = 0; k < NPT; ++k) {
         const int i = tid + k * NT;
         double acc = 0.0;
-        if (i < n) {
-            const Dec d = decompose_s(__ldg(s + i), n);
+        if (F || i < n) {
+            const Dec d = decompose_s(sv[k], n);
             double w[P + 1];
             lagrange_weights<P>(d.eps, w);
-            int j = d.e - SL;
-            if (j < 0) j += n;
+            const double *src = row + (d.e - SL);  // halo covers e-SL >= -3, e+R <= n+1
 #pragma unroll
             for (int c = 0; c <= P; ++c) {
-                const double prod = __dmul_rn(row[j], w[c]);
+                const double prod = __dmul_rn(src[c], w[c]);
                 acc = c == 0 ? prod : __dadd_rn(acc, prod);
-                j = (j + 1 == n) ? 0 : j + 1;
             }
         }
         v[k] = acc;
@@ -76,33 +133,38 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, const RowCtx &cx,
         return 0;
     } else {
         constexpr int RAD = (P + 1) / 2;
+        constexpr bool SIGREG = NPT <= 8 || NT <= 256;
+        const int64_t set = L.shared ? 0 : t;
         const double *sig = L.sig_x + set * (int64_t)n;
-
-        // (I - diag(sig) D) x  on the vector held in rowbuf, at node i
-        auto imsd_at = [&](int i, double xi) -> double {
+        double sg[SIGREG ? NPT : 1];
+        if constexpr (SIGREG) {
+#pragma unroll
+            for (int k = 0; k < NPT; ++k) {
+                const int i = tid + k * NT;
+                sg[k] = (F || i < n) ? __ldg(sig + i) : 0.0;
+            }
+        }
+        // (I - diag(sig) D) x at node i (k-th node of this thread) on rowbuf
+        auto imsd_at = [&](int k, int i, double xi) -> double {
             double acc;
             if constexpr (NUMBA) {
                 // _kernels.py:18-31: acc = sum_{k=-rad..rad} st[rad+k] * v[i+k]
                 acc = 0.0;
 #pragma unroll
-                for (int q = -RAD; q <= RAD; ++q) {
-                    int j = i + q;
-                    j = j < 0 ? j + n : (j >= n ? j - n : j);
-                    acc = __dadd_rn(acc, __dmul_rn(dcoef<P>(RAD + q), row[j]));
-                }
+                for (int q = -RAD; q <= RAD; ++q)
+                    acc = __dadd_rn(acc, __dmul_rn(dcoef<P>(RAD + q), row[i + q]));
             } else {
                 // coarse_correction.py:50-56: c0 v + sum_k (c_{+k} v_{i+k} + c_{-k} v_{i-k})
                 acc = __dmul_rn(dcoef<P>(RAD), xi);
 #pragma unroll
-                for (int q = 1; q <= RAD; ++q) {
-                    int jp = i + q, jm = i - q;
-                    jp = jp >= n ? jp - n : jp;
-                    jm = jm < 0 ? jm + n : jm;
-                    acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(dcoef<P>(RAD + q), row[jp]),
-                                                   __dmul_rn(dcoef<P>(RAD - q), row[jm])));
-                }
+                for (int q = 1; q <= RAD; ++q)
+                    acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(dcoef<P>(RAD + q), row[i + q]),
+                                                   __dmul_rn(dcoef<P>(RAD - q), row[i - q])));
             }
-            return __dsub_rn(xi, __dmul_rn(__ldg(sig + i), acc));
+            double s_i;
+            if constexpr (SIGREG) s_i = sg[k];
+            else s_i = __ldg(sig + i);
+            return __dsub_rn(xi, __dmul_rn(s_i, acc));
         };
 
         if constexpr (KIND == MGRIT_KIND_FORWARD_EULER) {
@@ -111,13 +173,13 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, const RowCtx &cx,
 #pragma unroll
             for (int k = 0; k < NPT; ++k) {
                 const int i = tid + k * NT;
-                if (i < n) cx.rowbuf[i] = v[k];
+                if (F || i < n) put_row(cx.rowbuf, i, v[k], n);
             }
             __syncthreads();
 #pragma unroll
             for (int k = 0; k < NPT; ++k) {
                 const int i = tid + k * NT;
-                if (i < n) v[k] = __dsub_rn(__dmul_rn(2.0, v[k]), imsd_at(i, v[k]));
+                if (F || i < n) v[k] = __dsub_rn(__dmul_rn(2.0, v[k]), imsd_at(k, i, v[k]));
             }
             return 0;
         } else {
@@ -126,33 +188,42 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, const RowCtx &cx,
             const int K = L.gmres_max_iters;
             const double tol = L.gmres_tol;
             GmresSmem &G = *cx.gs;
-            double *basis = cx.basis;
 
             // non-finite rhs -> NaN row + sticky flag (coarse_correction.py:181-182)
             int bad = 0;
 #pragma unroll
             for (int k = 0; k < NPT; ++k)
-                if (tid + k * NT < n && !isfinite(v[k])) bad = 1;
+                if ((F || tid + k * NT < n) && !isfinite(v[k])) bad = 1;
             if (__syncthreads_or(bad)) {
                 if (tid == 0) atomicExch(cx.status, 1);
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) v[k] = __longlong_as_double(0x7ff8000000000000LL);
                 return -1;
             }
-            double part = 0.0;
+            auto dot4 = [&](const double *b) -> double {
+                double a[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int k = 0; k < NPT; ++k) part = __dadd_rn(part, __dmul_rn(v[k], v[k]));
-            const double beta = sqrt(block_sum<NT>(part, cx.red));
+                for (int k = 0; k < NPT; ++k) {
+                    const int i = tid + k * NT;
+                    if (F || i < n) a[k & 3] = __dadd_rn(a[k & 3], __dmul_rn(b ? b[i] : v[k], v[k]));
+                }
+                return __dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3]));
+            };
+            const double beta = sqrt(block_sum2<NT>(dot4(nullptr), cx));
             if (beta == 0.0) {
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) v[k] = 0.0;
                 return 0;
             }
+            {
+                const double yb = 1.0 / beta;
+                double *b0 = cx.bvec(0, n);
 #pragma unroll
-            for (int k = 0; k < NPT; ++k) {
-                const int i = tid + k * NT;
-                v[k] = __ddiv_rn(v[k], beta);
-                if (i < n) basis[i] = v[k];
+                for (int k = 0; k < NPT; ++k) {
+                    const int i = tid + k * NT;
+                    v[k] = div_rcp(v[k], beta, yb);
+                    if (F || i < n) b0[i] = v[k];
+                }
             }
             if (tid == 0) {
                 G.g[0] = beta;
@@ -165,44 +236,59 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, const RowCtx &cx,
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) {
                     const int i = tid + k * NT;
-                    if (i < n) cx.rowbuf[i] = v[k];  // b_kk
+                    if (F || i < n) put_row(cx.rowbuf, i, v[k], n);  // b_kk
                 }
                 __syncthreads();
                 // w = A b_kk
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) {
                     const int i = tid + k * NT;
-                    v[k] = i < n ? imsd_at(i, row[i]) : 0.0;
+                    v[k] = (F || i < n) ? imsd_at(k, i, v[k]) : 0.0;
                 }
-                // modified Gram-Schmidt against b_0..b_kk
-#pragma unroll 1
-                for (int j = 0; j <= kk; ++j) {
-                    const double *bj = j == kk ? cx.rowbuf : basis + (int64_t)j * n;
-                    double pj = 0.0;
+                // modified Gram-Schmidt against b_0..b_kk (b_kk read from rowbuf);
+                // b_{j+1} is fetched into registers while b_j's reduction runs
+                double bc[NPT];
+                {
+                    const double *b0p = kk == 0 ? cx.rowbuf : cx.bvec(0, n);
 #pragma unroll
                     for (int k = 0; k < NPT; ++k) {
                         const int i = tid + k * NT;
-                        if (i < n) pj = __dadd_rn(pj, __dmul_rn(bj[i], v[k]));
+                        bc[k] = (F || i < n) ? b0p[i] : 0.0;
                     }
-                    const double h = block_sum<NT>(pj, cx.red);
+                }
+#pragma unroll 1
+                for (int j = 0; j <= kk; ++j) {
+                    double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int k = 0; k < NPT; ++k) a4[k & 3] = __dadd_rn(a4[k & 3], __dmul_rn(bc[k], v[k]));
+                    const double part = __dadd_rn(__dadd_rn(a4[0], a4[1]), __dadd_rn(a4[2], a4[3]));
+                    double bn[NPT];
+                    if (j < kk) {
+                        const double *bp = j + 1 == kk ? cx.rowbuf : cx.bvec(j + 1, n);
+#pragma unroll
+                        for (int k = 0; k < NPT; ++k) {
+                            const int i = tid + k * NT;
+                            bn[k] = (F || i < n) ? bp[i] : 0.0;
+                        }
+                    }
+                    const double h = block_sum2<NT>(part, cx);
                     if (tid == 0) G.H[j * kMaxKrylov + kk] = h;
 #pragma unroll
                     for (int k = 0; k < NPT; ++k) {
-                        const int i = tid + k * NT;
-                        if (i < n) v[k] = __dsub_rn(v[k], __dmul_rn(h, bj[i]));
+                        v[k] = __dsub_rn(v[k], __dmul_rn(h, bc[k]));
+                        bc[k] = bn[k];
                     }
                 }
-                double pn = 0.0;
-#pragma unroll
-                for (int k = 0; k < NPT; ++k) pn = __dadd_rn(pn, __dmul_rn(v[k], v[k]));
-                const double nrm = sqrt(block_sum<NT>(pn, cx.red));
+                const double nrm = sqrt(block_sum2<NT>(dot4(nullptr), cx));
                 const bool brk = nrm <= __dmul_rn(1e-14, beta);
                 if (!brk) {
+                    const double yn = 1.0 / nrm;
+                    double *bn = cx.bvec(kk + 1, n);
 #pragma unroll
                     for (int k = 0; k < NPT; ++k) {
                         const int i = tid + k * NT;
-                        v[k] = __ddiv_rn(v[k], nrm);
-                        if (i < n) basis[(int64_t)(kk + 1) * n + i] = v[k];
+                        v[k] = div_rcp(v[k], nrm, yn);
+                        if (F || i < n) bn[i] = v[k];
                     }
                 }
                 if (tid == 0) {
@@ -222,29 +308,29 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, const RowCtx &cx,
                     G.g[kk + 1] = __dmul_rn(-G.sn[kk], G.g[kk]);
                     G.g[kk] = __dmul_rn(G.cs[kk], G.g[kk]);
                     G.stop = brk || (tol >= 0.0 && fabs(G.g[kk + 1]) <= __dmul_rn(tol, beta));
+                    if (G.stop || kk + 1 == K) {
+                        // back substitution (_kernels.py:90-95)
+                        const int d = kk + 1;
+                        for (int j = d - 1; j >= 0; --j) {
+                            double acc = G.g[j];
+                            for (int jj = j + 1; jj < d; ++jj)
+                                acc = __dsub_rn(acc, __dmul_rn(h_(j, jj), G.y[jj]));
+                            G.y[j] = __ddiv_rn(acc, h_(j, j));
+                        }
+                    }
                 }
                 done = kk + 1;
                 __syncthreads();
                 if (G.stop) break;
             }
-            // back substitution (_kernels.py:90-95) on one thread
-            if (tid == 0) {
-                for (int j = done - 1; j >= 0; --j) {
-                    double acc = G.g[j];
-                    for (int jj = j + 1; jj < done; ++jj)
-                        acc = __dsub_rn(acc, __dmul_rn(G.H[j * kMaxKrylov + jj], G.y[jj]));
-                    G.y[j] = __ddiv_rn(acc, G.H[j * kMaxKrylov + j]);
-                }
-            }
-            __syncthreads();
             // x = sum_j b_j y_j (_kernels.py:96-101)
 #pragma unroll
             for (int k = 0; k < NPT; ++k) {
                 const int i = tid + k * NT;
                 double acc = 0.0;
-                if (i < n)
+                if (F || i < n)
                     for (int j = 0; j < done; ++j)
-                        acc = __dadd_rn(acc, __dmul_rn(basis[(int64_t)j * n + i], G.y[j]));
+                        acc = __dadd_rn(acc, __dmul_rn(cx.bvec(j, n)[i], G.y[j]));
                 v[k] = acc;
             }
             return done;
@@ -253,54 +339,54 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, const RowCtx &cx,
 }
 
 // store v into rowbuf (after a barrier protecting previous readers)
-template <int NT, int NPT>
+template <int NT, int NPT, bool F>
 __device__ __forceinline__ void set_row(double *rowbuf, const double (&v)[NPT], int n) {
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         const int i = threadIdx.x + k * NT;
-        if (i < n) rowbuf[i] = v[k];
+        if (F || i < n) put_row(rowbuf, i, v[k], n);
     }
     __syncthreads();
 }
 
-template <int NT, int NPT>
+template <int NT, int NPT, bool F>
 __device__ __forceinline__ void load_row(double (&v)[NPT], const double *src, int n) {
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         const int i = threadIdx.x + k * NT;
-        v[k] = i < n ? src[i] : 0.0;
+        v[k] = (F || i < n) ? src[i] : 0.0;
     }
 }
 
-template <int NT, int NPT>
+template <int NT, int NPT, bool F>
 __device__ __forceinline__ void store_row(double *dst, const double (&v)[NPT], int n) {
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         const int i = threadIdx.x + k * NT;
-        if (i < n) dst[i] = v[k];
+        if (F || i < n) dst[i] = v[k];
     }
 }
 
 // v += g (g NULL => + 0.0, keeping the reference's "+ G" rounding of -0.0)
-template <int NT, int NPT>
+template <int NT, int NPT, bool F>
 __device__ __forceinline__ void add_forcing(double (&v)[NPT], const double *g, int n) {
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         const int i = threadIdx.x + k * NT;
-        v[k] = __dadd_rn(v[k], (g && i < n) ? g[i] : 0.0);
+        v[k] = __dadd_rn(v[k], (g && (F || i < n)) ? g[i] : 0.0);
     }
 }
 
 // r = (g + v) - u ; returns this thread's sum of r^2
-template <int NT, int NPT>
+template <int NT, int NPT, bool F>
 __device__ __forceinline__ double residual_form(double (&v)[NPT], const double *g, const double *u,
                                                 int n) {
     double ss = 0.0;
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         const int i = threadIdx.x + k * NT;
-        if (i < n) {
+        if (F || i < n) {
             const double r = __dsub_rn(__dadd_rn(g ? g[i] : 0.0, v[k]), u[i]);
             v[k] = r;
             ss = __dadd_rn(ss, __dmul_rn(r, r));
@@ -311,14 +397,21 @@ __device__ __forceinline__ double residual_form(double (&v)[NPT], const double *
     return ss;
 }
 
-__device__ __forceinline__ RowCtx make_ctx(double *sm, int n, int NT, double *scratch,
-                                           int64_t slot, const mgrit_level_desc &L,
-                                           int32_t *status) {
+// dynamic shared memory: [halo | rowbuf n | halo][GmresSmem][nbs Krylov slots of n]
+__host__ __device__ inline size_t smem_bytes_for(int n, int nbs) {
+    return sizeof(double) * ((size_t)n + 2 * kHalo) + sizeof(GmresSmem) + sizeof(double) * (size_t)n * nbs;
+}
+
+__device__ __forceinline__ RowCtx make_ctx(double *sm, int n, int nbs, double *scratch, int64_t slot,
+                                           const mgrit_level_desc &L, int32_t *status) {
     RowCtx c;
-    c.rowbuf = sm;
-    c.red = sm + n;
-    c.gs = reinterpret_cast<GmresSmem *>(sm + n + NT / 32 + 1);
-    c.basis = scratch ? scratch + slot * (int64_t)(L.gmres_max_iters + 1) * n : nullptr;
+    c.rowbuf = sm + kHalo;
+    c.gs = reinterpret_cast<GmresSmem *>(sm + n + 2 * kHalo);
+    c.bsm = reinterpret_cast<double *>(c.gs + 1);
+    c.nbs = nbs;
+    const int spill = L.gmres_max_iters + 1 - nbs;
+    c.bgl = (scratch && spill > 0) ? scratch + slot * (int64_t)spill * n : nullptr;
+    c.sel = 0;
     c.status = status;
     return c;
 }
@@ -326,32 +419,32 @@ __device__ __forceinline__ RowCtx make_ctx(double *sm, int n, int NT, double *sc
 // ---------------------------------------------------------------------------
 // apply_rows: one CTA per row (persistent over rows)
 
-
-template <int P, int KIND, int NT, int NPT>
-__global__ void __launch_bounds__(NT) rows_kernel(mgrit_level_desc L, RowsArgs a, double *scratch,
+template <int P, int KIND, int NT, int NPT, bool F>
+__global__ void __launch_bounds__(NT) rows_kernel(mgrit_level_desc L, RowsArgs a, int nbs, double *scratch,
                                                   int32_t *status) {
     extern __shared__ double sm[];
     const int n = L.n_x;
-    RowCtx cx = make_ctx(sm, n, NT, scratch, blockIdx.x, L, status);
+    RowCtx cx = make_ctx(sm, n, nbs, scratch, blockIdx.x, L, status);
     for (int64_t b = blockIdx.x; b < a.B; b += gridDim.x) {
         const int64_t t = a.t_idx ? a.t_idx[b] : a.t_first + b * a.t_stride;
-        double v[NPT];
-        load_row<NT, NPT>(v, a.U_in + b * a.ld_in, n);
-        set_row<NT, NPT>(cx.rowbuf, v, n);
-        const int cnt = cta_apply<P, KIND, NT, NPT, false>(L, t, cx, v);
+        double v[NPT], sv[NPT];
+        load_records<NT, NPT, F>(L, t, sv);
+        load_row<NT, NPT, F>(v, a.U_in + b * a.ld_in, n);
+        set_row<NT, NPT, F>(cx.rowbuf, v, n);
+        const int cnt = cta_apply<P, KIND, NT, NPT, F, false>(L, t, cx, v, sv);
         const double *g = a.G ? a.G + b * a.ld_g : nullptr;
         double ss = 0.0;
         if (a.U_sub) {
-            ss = residual_form<NT, NPT>(v, g, a.U_sub + b * a.ld_sub, n);
+            ss = residual_form<NT, NPT, F>(v, g, a.U_sub + b * a.ld_sub, n);
         } else {
-            add_forcing<NT, NPT>(v, g, n);
+            add_forcing<NT, NPT, F>(v, g, n);
             if (a.row_sumsq)
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) ss = __dadd_rn(ss, __dmul_rn(v[k], v[k]));
         }
-        store_row<NT, NPT>(a.out + b * a.ld_out, v, n);
+        store_row<NT, NPT, F>(a.out + b * a.ld_out, v, n);
         if (a.row_sumsq) {
-            const double tot = block_sum<NT>(ss, cx.red);
+            const double tot = block_sum2<NT>(ss, cx);
             if (threadIdx.x == 0) a.row_sumsq[b] = tot;
         }
         if (a.gmres_iters && threadIdx.x == 0) a.gmres_iters[b] = cnt;
@@ -361,13 +454,14 @@ __global__ void __launch_bounds__(NT) rows_kernel(mgrit_level_desc L, RowsArgs a
 // ---------------------------------------------------------------------------
 // fused level phases: one CTA per C-interval (persistent over intervals)
 
-template <int P, int KIND, int NT, int NPT>
-__global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_phase_args A,
+template <int P, int KIND, int NT, int NPT, bool F>
+__global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_phase_args A, int nbs,
                                                    double *scratch, int32_t *status) {
     extern __shared__ double sm[];
+    constexpr bool PREFETCH = NPT <= 8;
     const int n = L.n_x;
     const int m = A.m;
-    RowCtx cx = make_ctx(sm, n, NT, scratch, blockIdx.x, L, status);
+    RowCtx cx = make_ctx(sm, n, nbs, scratch, blockIdx.x, L, status);
     auto U = [&](int64_t t) { return A.U + (t - A.u_row0) * A.ldu; };
     auto Gr = [&](int64_t t) -> const double * { return A.G ? A.G + (t - A.g_row0) * A.ldg : nullptr; };
     auto Cb = [&](int64_t c) { return A.Cbuf + (c - A.c_row0) * (int64_t)n; };
@@ -376,30 +470,31 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
     for (int64_t c = A.c_begin + blockIdx.x; c < A.c_begin + A.c_count; c += gridDim.x) {
         const int64_t t0 = c * m;
         const int64_t tC = t0 + m;
-        double v[NPT];
+        double v[NPT], sv[NPT];
+        load_records<NT, NPT, F>(L, t0, sv);
         // ---- left state of the interval
         const bool zero_left = A.zero_init && (c == 0 || A.phase == MGRIT_PHASE_FC ||
                                                A.phase == MGRIT_PHASE_FONLY_RES);
         if (zero_left) {
 #pragma unroll
             for (int k = 0; k < NPT; ++k) v[k] = 0.0;
-            if (c == 0 || A.phase == MGRIT_PHASE_FONLY_RES) store_row<NT, NPT>(U(t0), v, n);
+            if (c == 0 || A.phase == MGRIT_PHASE_FONLY_RES) store_row<NT, NPT, F>(U(t0), v, n);
         } else if (A.phase == MGRIT_PHASE_FC || A.phase == MGRIT_PHASE_FONLY_RES || c == 0) {
-            load_row<NT, NPT>(v, U(t0), n);
+            load_row<NT, NPT, F>(v, U(t0), n);
         } else {
-            load_row<NT, NPT>(v, Cb(c), n);
+            load_row<NT, NPT, F>(v, Cb(c), n);
         }
         if (A.phase == MGRIT_PHASE_INJ_F) {
             // U[::m] += Uc  (mgrit.py:333)
             double u[NPT];
-            load_row<NT, NPT>(u, Ucr(c), n);
+            load_row<NT, NPT, F>(u, Ucr(c), n);
 #pragma unroll
             for (int k = 0; k < NPT; ++k) v[k] = __dadd_rn(v[k], u[k]);
-            store_row<NT, NPT>(U(t0), v, n);
+            store_row<NT, NPT, F>(U(t0), v, n);
         } else if (A.phase == MGRIT_PHASE_F_RES && c > 0) {
-            store_row<NT, NPT>(U(t0), v, n);
+            store_row<NT, NPT, F>(U(t0), v, n);
         }
-        set_row<NT, NPT>(cx.rowbuf, v, n);
+        set_row<NT, NPT, F>(cx.rowbuf, v, n);
 
         // ---- F-relaxation chain (mgrit.py:276-283) then the interval tail at
         //      k == m; a single call site of the step operator keeps the
@@ -409,50 +504,60 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
         if (A.phase == MGRIT_PHASE_INJ_F && !A.partial && last) {
             // U[N] += Uc[N/m] for the final C-point (mgrit.py:333)
             double right[NPT], u[NPT];
-            load_row<NT, NPT>(right, Cb(c + 1), n);
-            load_row<NT, NPT>(u, Ucr(c + 1), n);
+            load_row<NT, NPT, F>(right, Cb(c + 1), n);
+            load_row<NT, NPT, F>(u, Ucr(c + 1), n);
 #pragma unroll
             for (int k = 0; k < NPT; ++k) right[k] = __dadd_rn(right[k], u[k]);
-            store_row<NT, NPT>(U(tC), right, n);
+            store_row<NT, NPT, F>(U(tC), right, n);
         }
 #pragma unroll 1
         for (int k = 1; k <= kmax; ++k) {
             const int64_t t = t0 + k;
-            cta_apply<P, KIND, NT, NPT, false>(L, t - 1, cx, v);
+            double sn[PREFETCH ? NPT : 1];
+            if constexpr (PREFETCH) {
+                if (k < kmax) load_records<NT, NPT, F>(L, t, sn);
+            }
+            cta_apply<P, KIND, NT, NPT, F, false>(L, t - 1, cx, v, sv);
+            if constexpr (PREFETCH) {
+#pragma unroll
+                for (int q = 0; q < NPT; ++q) sv[q] = sn[q];
+            } else {
+                if (k < kmax) load_records<NT, NPT, F>(L, t, sv);
+            }
             if (k < m) {
-                add_forcing<NT, NPT>(v, Gr(t), n);
-                store_row<NT, NPT>(U(t), v, n);
-                set_row<NT, NPT>(cx.rowbuf, v, n);
+                add_forcing<NT, NPT, F>(v, Gr(t), n);
+                store_row<NT, NPT, F>(U(t), v, n);
+                set_row<NT, NPT, F>(cx.rowbuf, v, n);
                 continue;
             }
             // ---- interval tail at the right C-point tC = t
             if (A.phase == MGRIT_PHASE_FC) {
                 // C-relaxation (mgrit.py:286-290) into the C-point buffer
-                add_forcing<NT, NPT>(v, Gr(tC), n);
-                store_row<NT, NPT>(Cb(c + 1), v, n);
+                add_forcing<NT, NPT, F>(v, Gr(tC), n);
+                store_row<NT, NPT, F>(Cb(c + 1), v, n);
                 break;
             }
             // subtrahend of the C-point residual: the current U[tC]
             double right[NPT];
             if (A.phase == MGRIT_PHASE_INJ_F) {
                 double u[NPT];
-                load_row<NT, NPT>(right, Cb(c + 1), n);
-                load_row<NT, NPT>(u, Ucr(c + 1), n);
+                load_row<NT, NPT, F>(right, Cb(c + 1), n);
+                load_row<NT, NPT, F>(u, Ucr(c + 1), n);
 #pragma unroll
                 for (int q = 0; q < NPT; ++q) right[q] = __dadd_rn(right[q], u[q]);
-                if (last) store_row<NT, NPT>(U(tC), right, n);
+                if (last) store_row<NT, NPT, F>(U(tC), right, n);
             } else if (A.phase == MGRIT_PHASE_F_RES) {
-                load_row<NT, NPT>(right, Cb(c + 1), n);
-                store_row<NT, NPT>(U(tC), right, n);
+                load_row<NT, NPT, F>(right, Cb(c + 1), n);
+                store_row<NT, NPT, F>(U(tC), right, n);
             } else {  // FONLY_RES
                 if (A.zero_init) {
 #pragma unroll
                     for (int q = 0; q < NPT; ++q) right[q] = 0.0;
-                    store_row<NT, NPT>(U(tC), right, n);
+                    store_row<NT, NPT, F>(U(tC), right, n);
                 } else {
-                    load_row<NT, NPT>(right, U(tC), n);
+                    load_row<NT, NPT, F>(right, U(tC), n);
                 }
-                store_row<NT, NPT>(Cb(c + 1), right, n);
+                store_row<NT, NPT, F>(Cb(c + 1), right, n);
             }
             // r = (G + Phi U[tC-1]) - U[tC]; F-point residuals are exactly 0
             // after F-relaxation ((G + S) - (S + G) == 0 bitwise), so the
@@ -462,16 +567,16 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
 #pragma unroll
             for (int q = 0; q < NPT; ++q) {
                 const int i = threadIdx.x + q * NT;
-                if (i < n) {
+                if (F || i < n) {
                     const double r = __dsub_rn(__dadd_rn(g ? g[i] : 0.0, v[q]), right[q]);
                     v[q] = r;
                     ss = __dadd_rn(ss, __dmul_rn(r, r));
                 }
             }
             if (A.Gc && A.phase != MGRIT_PHASE_INJ_F)
-                store_row<NT, NPT>(A.Gc + (c + 1 - A.c_row0) * (int64_t)n, v, n);
+                store_row<NT, NPT, F>(A.Gc + (c + 1 - A.c_row0) * (int64_t)n, v, n);
             if (A.partial) {
-                const double tot = block_sum<NT>(ss, cx.red);
+                const double tot = block_sum2<NT>(ss, cx);
                 if (threadIdx.x == 0) A.partial[c - A.partial0] = tot;
             }
         }
@@ -481,47 +586,78 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
 // ---------------------------------------------------------------------------
 // sequential sweep: one CTA steps the whole level
 
-template <int P, int KIND, int NT, int NPT, bool NUMBA>
+template <int P, int KIND, int NT, int NPT, bool F, bool NUMBA>
 __global__ void __launch_bounds__(NT) sweep_kernel(mgrit_level_desc L, double *U, int64_t ldu,
                                                    const double *G, int64_t ldg, int zero_init,
-                                                   int32_t *gmres_iters, double *scratch,
+                                                   int32_t *gmres_iters, int nbs, double *scratch,
                                                    int32_t *status) {
     extern __shared__ double sm[];
+    constexpr bool PREFETCH = NPT <= 8;
     const int n = L.n_x;
-    RowCtx cx = make_ctx(sm, n, NT, scratch, 0, L, status);
-    double v[NPT];
+    RowCtx cx = make_ctx(sm, n, nbs, scratch, 0, L, status);
+    double v[NPT], sv[NPT];
+    load_records<NT, NPT, F>(L, 0, sv);
     if (zero_init) {
 #pragma unroll
         for (int k = 0; k < NPT; ++k) v[k] = 0.0;
-        store_row<NT, NPT>(U, v, n);
+        store_row<NT, NPT, F>(U, v, n);
     } else {
-        load_row<NT, NPT>(v, U, n);
+        load_row<NT, NPT, F>(v, U, n);
     }
-    set_row<NT, NPT>(cx.rowbuf, v, n);
+    set_row<NT, NPT, F>(cx.rowbuf, v, n);
+#pragma unroll 1
     for (int64_t t = 0; t < L.n_steps; ++t) {
-        const int cnt = cta_apply<P, KIND, NT, NPT, NUMBA>(L, t, cx, v);
-        add_forcing<NT, NPT>(v, G ? G + (t + 1) * ldg : nullptr, n);
-        store_row<NT, NPT>(U + (t + 1) * ldu, v, n);
+        double sn[PREFETCH ? NPT : 1];
+        if constexpr (PREFETCH) {
+            if (t + 1 < L.n_steps) load_records<NT, NPT, F>(L, t + 1, sn);
+        }
+        const int cnt = cta_apply<P, KIND, NT, NPT, F, NUMBA>(L, t, cx, v, sv);
+        if constexpr (PREFETCH) {
+#pragma unroll
+            for (int q = 0; q < NPT; ++q) sv[q] = sn[q];
+        } else {
+            if (t + 1 < L.n_steps) load_records<NT, NPT, F>(L, t + 1, sv);
+        }
+        add_forcing<NT, NPT, F>(v, G ? G + (t + 1) * ldg : nullptr, n);
+        store_row<NT, NPT, F>(U + (t + 1) * ldu, v, n);
         if (gmres_iters && threadIdx.x == 0) gmres_iters[t] = cnt;
-        set_row<NT, NPT>(cx.rowbuf, v, n);
+        set_row<NT, NPT, F>(cx.rowbuf, v, n);
     }
 }
 
 // ---------------------------------------------------------------------------
-// launch configuration: a CTA owns a whole row, NPT <= 16 nodes per thread
+// launch configuration: a CTA owns a whole row
 
 struct Cfg1D {
     int nt, npt;
 };
 
-static Cfg1D cfg_for(int n) {
-    if (n <= 2048) return {128, 16};
-    if (n <= 4096) return {256, 16};
-    if (n <= 8192) return {512, 16};
-    return {512, 32};
+inline Cfg1D cfg_for(int n) {
+    if (n <= 1024) return {256, 4};
+    if (n <= 2048) return {512, 4};
+    if (n <= 4096) return {1024, 4};
+    if (n <= 8192) return {1024, 8};
+    return {1024, 16};
 }
 
-static int resident_ctas(const void *fn, int nt, size_t smem) {
+inline int max_smem_optin() {
+    int dev = 0, v = 48 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+}
+
+// Krylov slots that fit in shared memory next to the row
+inline int smem_slots(const mgrit_level_desc *L) {
+    if (L->kind != MGRIT_KIND_CORRECTED) return 0;
+    const int64_t base = (int64_t)smem_bytes_for(L->n_x, 0);
+    const int64_t avail = (int64_t)max_smem_optin() - base - 1024;
+    int64_t k = avail > 0 ? avail / ((int64_t)L->n_x * 8) : 0;
+    if (k > L->gmres_max_iters + 1) k = L->gmres_max_iters + 1;
+    return (int)(k < 0 ? 0 : k);
+}
+
+inline int resident_ctas(const void *fn, int nt, size_t smem) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -531,8 +667,7 @@ static int resident_ctas(const void *fn, int nt, size_t smem) {
 }
 
 template <typename F>
-static int prep(F fn, size_t smem) {
-    static_assert(sizeof(F) > 0, "");
+inline int prep(F fn, size_t smem) {
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -544,21 +679,39 @@ static int prep(F fn, size_t smem) {
     return MGRIT_OK;
 }
 
-template <int P_, int KIND_, int NT_, int NPT_>
+template <int P_, int KIND_, int NT_, int NPT_, bool F_>
 struct Tag {
     static constexpr int P = P_, KIND = KIND_, NT = NT_, NPT = NPT_;
+    static constexpr bool F = F_;  // n == NT * NPT: no bounds checks
 };
 
-template <int P, int KIND, typename F>
-static int dispatch_cfg(Cfg1D c, F &&f) {
-    if (c.nt <= 128) return f(Tag<P, KIND, 128, 16>{});
-    if (c.nt <= 256) return f(Tag<P, KIND, 256, 16>{});
-    if (c.npt <= 16) return f(Tag<P, KIND, 512, 16>{});
-    return f(Tag<P, KIND, 512, 32>{});
+// full rows (n == NT*NPT: the power-of-two meshes of every BASELINE config)
+// compile without bounds checks; any other n uses a checked variant.
+// Plain SL / forward-Euler steps are HBM/issue bound: 1024 threads x 4 nodes
+// keep the most loads in flight.  Corrected (GMRES) steps are bound by the
+// latency of ~K^2/2 dependent block reductions whose instruction cost scales
+// with the warp count: 256 threads x n/256 nodes minimise it.
+template <int P, int KIND, typename Fn>
+static int dispatch_cfg(Cfg1D, int n, Fn &&f) {
+    if constexpr (KIND == MGRIT_KIND_CORRECTED) {
+        if (n == 1024) return f(Tag<P, KIND, 256, 4, true>{});
+        if (n == 2048) return f(Tag<P, KIND, 256, 8, true>{});
+        if (n == 4096) return f(Tag<P, KIND, 256, 16, true>{});
+        if (n == 8192) return f(Tag<P, KIND, 512, 16, true>{});
+        if (n == 16384) return f(Tag<P, KIND, 1024, 16, true>{});
+    } else {
+        if (n == 1024) return f(Tag<P, KIND, 256, 4, true>{});
+        if (n == 2048) return f(Tag<P, KIND, 512, 4, true>{});
+        if (n == 4096) return f(Tag<P, KIND, 1024, 4, true>{});
+        if (n == 8192) return f(Tag<P, KIND, 1024, 8, true>{});
+        if (n == 16384) return f(Tag<P, KIND, 1024, 16, true>{});
+    }
+    if (n < 1024) return f(Tag<P, KIND, 256, 4, false>{});
+    return f(Tag<P, KIND, 1024, 16, false>{});
 }
 
 inline int validate(const mgrit_level_desc *L) {
-    if (!L || L->dim != 1 || L->n_x < 1 || L->n_x > 16384 || !L->s_x) return MGRIT_EINVAL;
+    if (!L || L->dim != 1 || L->n_x < 8 || L->n_x > 16384 || !L->s_x) return MGRIT_EINVAL;
     if (L->p != 1 && L->p != 3 && L->p != 5) return MGRIT_EINVAL;
     if (L->kind < 0 || L->kind > 2) return MGRIT_EINVAL;
     if (L->kind != MGRIT_KIND_SL && !L->sig_x) return MGRIT_EINVAL;
@@ -567,8 +720,11 @@ inline int validate(const mgrit_level_desc *L) {
     return MGRIT_OK;
 }
 
+// global Krylov bytes one CTA needs beyond its shared-memory slots
 inline int64_t scratch_per_cta(const mgrit_level_desc *L) {
-    return L->kind == MGRIT_KIND_CORRECTED ? (int64_t)(L->gmres_max_iters + 1) * L->n_x * 8 : 0;
+    if (L->kind != MGRIT_KIND_CORRECTED) return 0;
+    const int spill = L->gmres_max_iters + 1 - smem_slots(L);
+    return spill > 0 ? (int64_t)spill * L->n_x * 8 : 0;
 }
 
 inline int cap_grid(int64_t want, int resident, const mgrit_level_desc *L, int64_t scratch_bytes) {
@@ -580,7 +736,6 @@ inline int cap_grid(int64_t want, int resident, const mgrit_level_desc *L, int64
     }
     return (int)g;
 }
-
 
 // Host launchers for one (P, KIND); explicitly instantiated one pair per
 // translation unit (step1d_p*_k*.cu) so the heavy kernel bodies compile in
@@ -601,29 +756,33 @@ struct Launch1D {
 template <int P, int KIND>
 int64_t Launch1D<P, KIND>::capacity(const mgrit_level_desc *L) {
     const Cfg1D c = cfg_for(L->n_x);
-    const size_t smem = smem_bytes_for(L->n_x, c.nt);
-    return dispatch_cfg<P, KIND>(c, [&](auto T) {
+    const int nbs = smem_slots(L);
+    const size_t smem = smem_bytes_for(L->n_x, nbs);
+    return dispatch_cfg<P, KIND>(c, L->n_x, [&](auto T) {
         using C = decltype(T);
-        return resident_ctas((const void *)rows_kernel<C::P, C::KIND, C::NT, C::NPT>, C::NT, smem);
+        auto fn = rows_kernel<C::P, C::KIND, C::NT, C::NPT, C::F>;
+        if (prep(fn, smem)) return 1;
+        return resident_ctas((const void *)fn, C::NT, smem);
     });
 }
 
 template <int P, int KIND>
 int Launch1D<P, KIND>::rows(const mgrit_level_desc *L, const RowsArgs &a, void *scratch,
-                  int64_t scratch_bytes, int32_t *status, cudaStream_t st) {
+                            int64_t scratch_bytes, int32_t *status, cudaStream_t st) {
     int rc = validate(L);
     if (rc) return rc;
     if (a.B <= 0) return MGRIT_OK;
     const Cfg1D c = cfg_for(L->n_x);
-    const size_t smem = smem_bytes_for(L->n_x, c.nt);
-    rc = dispatch_cfg<P, KIND>(c, [&](auto T) {
+    const int nbs = smem_slots(L);
+    const size_t smem = smem_bytes_for(L->n_x, nbs);
+    rc = dispatch_cfg<P, KIND>(c, L->n_x, [&](auto T) {
         using C = decltype(T);
-        auto fn = rows_kernel<C::P, C::KIND, C::NT, C::NPT>;
+        auto fn = rows_kernel<C::P, C::KIND, C::NT, C::NPT, C::F>;
         int r = prep(fn, smem);
         if (r) return r;
         const int grid = cap_grid(a.B, resident_ctas((const void *)fn, C::NT, smem), L, scratch_bytes);
         if (grid < 1) return (int)MGRIT_EINVAL;
-        fn<<<grid, C::NT, smem, st>>>(*L, a, (double *)scratch, status);
+        fn<<<grid, C::NT, smem, st>>>(*L, a, nbs, (double *)scratch, status);
         return (int)MGRIT_OK;
     });
     if (rc) return rc;
@@ -632,7 +791,7 @@ int Launch1D<P, KIND>::rows(const mgrit_level_desc *L, const RowsArgs &a, void *
 
 template <int P, int KIND>
 int Launch1D<P, KIND>::phase(const mgrit_level_desc *L, const mgrit_phase_args *A, void *scratch,
-                   int64_t scratch_bytes, int32_t *status, cudaStream_t st) {
+                             int64_t scratch_bytes, int32_t *status, cudaStream_t st) {
     int rc = validate(L);
     if (rc) return rc;
     if (!A || A->m < 1 || !A->U || A->c_count < 0 || A->n_intervals < 1) return MGRIT_EINVAL;
@@ -642,15 +801,16 @@ int Launch1D<P, KIND>::phase(const mgrit_level_desc *L, const mgrit_phase_args *
     if (A->phase == MGRIT_PHASE_INJ_F && !A->Uc) return MGRIT_EINVAL;
     if (A->c_count == 0) return MGRIT_OK;
     const Cfg1D c = cfg_for(L->n_x);
-    const size_t smem = smem_bytes_for(L->n_x, c.nt);
-    rc = dispatch_cfg<P, KIND>(c, [&](auto T) {
+    const int nbs = smem_slots(L);
+    const size_t smem = smem_bytes_for(L->n_x, nbs);
+    rc = dispatch_cfg<P, KIND>(c, L->n_x, [&](auto T) {
         using C = decltype(T);
-        auto fn = phase_kernel<C::P, C::KIND, C::NT, C::NPT>;
+        auto fn = phase_kernel<C::P, C::KIND, C::NT, C::NPT, C::F>;
         int r = prep(fn, smem);
         if (r) return r;
         const int grid = cap_grid(A->c_count, resident_ctas((const void *)fn, C::NT, smem), L, scratch_bytes);
         if (grid < 1) return (int)MGRIT_EINVAL;
-        fn<<<grid, C::NT, smem, st>>>(*L, *A, (double *)scratch, status);
+        fn<<<grid, C::NT, smem, st>>>(*L, *A, nbs, (double *)scratch, status);
         return (int)MGRIT_OK;
     });
     if (rc) return rc;
@@ -658,30 +818,32 @@ int Launch1D<P, KIND>::phase(const mgrit_level_desc *L, const mgrit_phase_args *
 }
 
 template <int P, int KIND>
-int Launch1D<P, KIND>::sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg,
-             int zero_init, int32_t *gmres_iters, void *scratch, int64_t scratch_bytes,
-             int32_t *status, cudaStream_t st) {
+int Launch1D<P, KIND>::sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G,
+                             int64_t ldg, int zero_init, int32_t *gmres_iters, void *scratch,
+                             int64_t scratch_bytes, int32_t *status, cudaStream_t st) {
     int rc = validate(L);
     if (rc) return rc;
     if (!U) return MGRIT_EINVAL;
     if (scratch_per_cta(L) > scratch_bytes) return MGRIT_EINVAL;
     const Cfg1D c = cfg_for(L->n_x);
-    const size_t smem = smem_bytes_for(L->n_x, c.nt);
+    const int nbs = smem_slots(L);
+    const size_t smem = smem_bytes_for(L->n_x, nbs);
     const bool numba = L->stencil_numba && L->kind == MGRIT_KIND_CORRECTED;
-    rc = dispatch_cfg<P, KIND>(c, [&](auto T) {
+    rc = dispatch_cfg<P, KIND>(c, L->n_x, [&](auto T) {
         using C = decltype(T);
         int r;
         if constexpr (C::KIND == MGRIT_KIND_CORRECTED) {
             if (numba) {
-                auto fn = sweep_kernel<C::P, C::KIND, C::NT, C::NPT, true>;
+                auto fn = sweep_kernel<C::P, C::KIND, C::NT, C::NPT, C::F, true>;
                 if ((r = prep(fn, smem))) return r;
-                fn<<<1, C::NT, smem, st>>>(*L, U, ldu, G, ldg, zero_init, gmres_iters, (double *)scratch, status);
+                fn<<<1, C::NT, smem, st>>>(*L, U, ldu, G, ldg, zero_init, gmres_iters, nbs, (double *)scratch,
+                                           status);
                 return (int)MGRIT_OK;
             }
         }
-        auto fn = sweep_kernel<C::P, C::KIND, C::NT, C::NPT, false>;
+        auto fn = sweep_kernel<C::P, C::KIND, C::NT, C::NPT, C::F, false>;
         if ((r = prep(fn, smem))) return r;
-        fn<<<1, C::NT, smem, st>>>(*L, U, ldu, G, ldg, zero_init, gmres_iters, (double *)scratch, status);
+        fn<<<1, C::NT, smem, st>>>(*L, U, ldu, G, ldg, zero_init, gmres_iters, nbs, (double *)scratch, status);
         return (int)MGRIT_OK;
     });
     if (rc) return rc;

@@ -629,13 +629,15 @@ def initial_state(cfg: SolverConfig, grid) -> np.ndarray:
 
 
 def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_iterate=None,
-          output: str = "numpy", use_graph: bool = True, engine: str = "auto"):
+          output: str = "numpy", out=None, use_graph: bool = True, engine: str = "auto"):
     """Run MGRIT (mgrit.py:337-378) on the device.
 
     ``initial_iterate``: optional host array (n_t, n_points) uploaded as U[1:];
     by default U[1:] is numpy's ``default_rng(seed).random`` stream generated
     bit-identically on the device (``iterate="pm1"`` maps it to [-1, 1)).
     ``output``: "numpy" (reference behaviour, host copy of U) or "device".
+    ``out``: optional preallocated host buffer (numpy array or pinned torch
+    CPU tensor) of shape (n_t + 1, n_points) receiving U; returned as numpy.
     ``engine``: "fused" (default when supported), "reference" (the
     reference-structured v_cycle built from batched launches).
     """
@@ -713,13 +715,18 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
             if r <= cfg.rtol * r0:
                 state = "converged"
                 break
-    out = U.cpu().numpy() if output == "numpy" else U
+    if out is not None:
+        dst = torch.from_numpy(out) if isinstance(out, np.ndarray) else out
+        dst.copy_(U)
+        result = dst.numpy()
+    else:
+        result = U.cpu().numpy() if output == "numpy" else U
     torch.cuda.synchronize()
     t_end = time.perf_counter()
     hist = np.array(history)
     factor = float(hist[-1] / hist[-2]) if len(hist) > 1 else float("nan")
     rep = ConvergenceReport(hist, len(hist) - 1, state, factor, t_end - t_begin, t_setup, t_end - t_solve0)
-    return rep, out
+    return rep, result
 
 
 def _capture(fn):

@@ -1,0 +1,333 @@
+"""Time-parallel MGRIT across ranks (one process per GPU).
+
+The time axis of every level is split into contiguous blocks of whole
+C-intervals; rank r owns intervals [r*I/P, (r+1)*I/P) of a level with
+I = n_steps/m intervals, i.e. the state rows of global steps
+[r*I/P*m, (r+1)*I/P*m] (its left boundary C-point included).  Because
+n_steps(l+1) = I(l), the coarse level's rank-r rows are exactly the fine
+level's C-indices of rank r, so restriction (Gc = R[::m]) and injection
+(U[::m] += Uc) never cross ranks.
+
+The only data that moves per sharded level and V-cycle:
+  * after F+C relaxation: the C-point buffer row at the block's right edge
+    goes to the right neighbour (its F-relaxation starts there);
+  * after injection + F-relaxation: the freshly injected left-edge C-point row
+    goes to the left neighbour (it is that rank's right edge).
+One state row each (8 n bytes), NCCL send/recv over NVLink.  The
+convergence norm all-gathers the per-interval partial sums and every rank
+adds them in global interval order, so histories are bitwise independent
+of P.  Levels whose interval count is not divisible by P, and always the
+coarsest level, are replicated: their forcing is all-gathered and every
+rank runs the remaining hierarchy redundantly (no further communication).
+
+The engine is written against a small backend interface (``phase``,
+``sweep``, ``total``) so the same sharding / exchange logic runs on the
+CUDA kernels (``CudaPhaseBackend``, product) and, in the CPU test-suite, on
+a numpy restatement of the phase semantics over gloo.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+# ---------------------------------------------------------------------------
+# communication
+
+
+class Comm:
+    """Neighbour shifts and all-gathers over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.size = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def _global(self, r):
+        return dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def shift(self, send: torch.Tensor | None, recv: torch.Tensor | None, direction: int):
+        """direction=+1: rank r sends to r+1 and receives from r-1; -1 reverses."""
+        if self.size == 1:
+            return
+        ops = []
+        dst, src = self.rank + direction, self.rank - direction
+        if send is not None and 0 <= dst < self.size:
+            ops.append(dist.P2POp(dist.isend, send, self._global(dst), self.group))
+        if recv is not None and 0 <= src < self.size:
+            ops.append(dist.P2POp(dist.irecv, recv, self._global(src), self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def allgather(self, full: torch.Tensor, local: torch.Tensor):
+        if self.size == 1:
+            full.copy_(local)
+            return
+        dist.all_gather_into_tensor(full, local.contiguous(), group=self.group)
+
+
+# ---------------------------------------------------------------------------
+# plan
+
+
+@dataclass
+class LevelPlan:
+    n_steps: int
+    m: int | None          # coarsening factor toward the next level (None: coarsest)
+    sharded: bool
+    cb: int = 0            # first owned interval (sharded) / 0
+    ce: int = 0            # one past the last owned interval
+    row0: int = 0          # global step of local row 0
+
+    @property
+    def n_intervals(self):
+        return self.n_steps // self.m if self.m else 0
+
+    @property
+    def local_rows(self):
+        return (self.ce - self.cb) * self.m + 1 if self.sharded else self.n_steps + 1
+
+
+def make_plan(sizes: list[int], factors: list[int | None], rank: int, size: int) -> list[LevelPlan]:
+    """Shard each level while its interval count divides by P (and every finer
+    level is sharded); the remaining coarse levels are replicated."""
+    plans = []
+    chain = True
+    for N, m in zip(sizes, factors):
+        if m is None:
+            plans.append(LevelPlan(N, None, False))
+            continue
+        I = N // m
+        chain = chain and I % size == 0
+        if chain:
+            cb, ce = rank * I // size, (rank + 1) * I // size
+            plans.append(LevelPlan(N, m, True, cb, ce, cb * m))
+        else:
+            plans.append(LevelPlan(N, m, False, 0, I, 0))
+    return plans
+
+
+# ---------------------------------------------------------------------------
+# CUDA backend (product)
+
+
+class CudaPhaseBackend:
+    """Launches the fused phase kernels / sweep of libmgrit_b200.so."""
+
+    def __init__(self, levels):
+        from .mgrit import _WS
+        self.levels = levels
+        self.lib = _lib.load()
+        self.descs = [lv.desc() for lv in levels[:-1]]
+        self.desc_last = levels[-1].desc(stencil_numba=levels[-1].stencil_numba)
+        dev = levels[0].device
+        need = 0
+        for lv, d in zip(levels[:-1], self.descs):
+            rows = min(lv.n_steps // lv.cf, max(1, int(self.lib.mgrit_resident_rows(ctypes.byref(d)))))
+            need = max(need, int(self.lib.mgrit_gmres_scratch_bytes(ctypes.byref(d), rows)))
+        need = max(need, int(self.lib.mgrit_gmres_scratch_bytes(ctypes.byref(self.desc_last), 1)))
+        self.scratch = torch.empty(max(need, 8), dtype=torch.uint8, device=dev)
+        self.status = _WS.get_status(dev)
+
+    @staticmethod
+    def _stream():
+        return torch.cuda.current_stream().cuda_stream
+
+    def phase(self, li, phase, *, m, c_begin, c_count, n_intervals, U, u_row0, G, g_row0, Cbuf, Uc, Gc,
+              c_row0, partial, partial0, zero_init):
+        a = _lib.PhaseArgs()
+        n = self.levels[li].grid.n_points
+        a.phase, a.m = phase, m
+        a.c_begin, a.c_count, a.n_intervals = c_begin, c_count, n_intervals
+        a.U, a.ldu, a.u_row0 = U.data_ptr(), n, u_row0
+        a.G, a.ldg, a.g_row0 = (0 if G is None else G.data_ptr()), n, g_row0
+        a.Cbuf = Cbuf.data_ptr()
+        a.Uc = 0 if Uc is None else Uc.data_ptr()
+        a.Gc = 0 if Gc is None else Gc.data_ptr()
+        a.c_row0 = c_row0
+        a.partial = 0 if partial is None else partial.data_ptr()
+        a.partial0 = partial0
+        a.zero_init = int(zero_init)
+        rc = self.lib.mgrit_level_phase(ctypes.byref(self.descs[li]), ctypes.byref(a), self.scratch.data_ptr(),
+                                        self.scratch.numel(), self.status.data_ptr(), self._stream())
+        _lib.check(rc, "level_phase")
+
+    def sweep(self, li, U, G, zero_init):
+        n = self.levels[li].grid.n_points
+        rc = self.lib.mgrit_sequential_sweep(ctypes.byref(self.desc_last), U.data_ptr(), n,
+                                             0 if G is None else G.data_ptr(), n, int(zero_init), 0,
+                                             self.scratch.data_ptr(), self.scratch.numel(),
+                                             self.status.data_ptr(), self._stream())
+        _lib.check(rc, "sequential_sweep")
+
+    def total(self, x: torch.Tensor, out: torch.Tensor):
+        _lib.check(self.lib.mgrit_sum(x.data_ptr(), x.numel(), out.data_ptr(), self._stream()), "sum")
+
+    def bad(self) -> bool:
+        return int(self.status.item()) != 0
+
+
+# ---------------------------------------------------------------------------
+# engine
+
+
+class TimeParallelCycle:
+    """Buffers and launch/exchange sequence of one sharded V-cycle."""
+
+    def __init__(self, plans: list[LevelPlan], n_points: int, backend, comm: Comm, relaxation: str,
+                 U0: torch.Tensor, device, dtype=torch.float64):
+        self.plans, self.n, self.be, self.comm, self.relax = plans, n_points, backend, comm, relaxation
+        L = len(plans)
+        z = lambda rows: torch.zeros((rows, n_points), dtype=dtype, device=device)  # noqa: E731
+        self.U = [U0] + [z(p.local_rows) for p in plans[1:]]
+        self.G = [None] + [z(p.local_rows) for p in plans[1:]]
+        self.C = [z(p.ce - p.cb + 1) for p in plans[:-1]]
+        # restriction target of a sharded level whose child is replicated: a local
+        # slab (row 0 unused) that is all-gathered into the child's full G
+        self.Gslab = [None] * L
+        for li in range(L - 1):
+            if plans[li].sharded and not plans[li + 1].sharded:
+                self.Gslab[li] = z(plans[li].ce - plans[li].cb + 1)
+        p0 = plans[0]
+        self.partial = torch.zeros(p0.ce - p0.cb, dtype=dtype, device=device)
+        self.partial_all = torch.zeros(p0.n_intervals, dtype=dtype, device=device)
+        self.sumsq = torch.zeros(1, dtype=dtype, device=device)
+
+    def _args(self, li, phase, zero_init):
+        p, c = self.plans[li], self.plans[li + 1]
+        Gc = None
+        if phase in (_lib.PHASE_F_RES, _lib.PHASE_FONLY_RES):
+            Gc = self.Gslab[li] if self.Gslab[li] is not None else self.G[li + 1]
+        # the child's U/G local row 0 is global C-index c.row0 (== p.cb when both
+        # are sharded, 0 when the child is replicated); Uc is indexed from p.cb
+        Uc = self.U[li + 1] if c.sharded else self.U[li + 1][p.cb:]
+        return dict(m=p.m, c_begin=p.cb, c_count=p.ce - p.cb, n_intervals=p.n_intervals, U=self.U[li],
+                    u_row0=p.row0, G=self.G[li], g_row0=p.row0, Cbuf=self.C[li], Uc=Uc, Gc=Gc, c_row0=p.cb,
+                    partial=self.partial if (li == 0 and phase == _lib.PHASE_INJ_F) else None, partial0=p.cb,
+                    zero_init=zero_init)
+
+    def cycle(self, li: int = 0):
+        plans, be, comm = self.plans, self.be, self.comm
+        p = plans[li]
+        zero = li > 0
+        if p.m is None:
+            be.sweep(li, self.U[li], self.G[li], zero_init=zero)
+            return
+        last_local = p.ce - p.cb
+        if self.relax == "FCF":
+            be.phase(li, _lib.PHASE_FC, **self._args(li, _lib.PHASE_FC, zero))
+            if p.sharded:
+                comm.shift(self.C[li][last_local], self.C[li][0], +1)
+            be.phase(li, _lib.PHASE_F_RES, **self._args(li, _lib.PHASE_F_RES, zero))
+        else:
+            be.phase(li, _lib.PHASE_FONLY_RES, **self._args(li, _lib.PHASE_FONLY_RES, zero))
+            if p.sharded:
+                comm.shift(self.C[li][last_local], self.C[li][0], +1)
+        if self.Gslab[li] is not None:
+            comm.allgather(self.G[li + 1][1:], self.Gslab[li][1:])
+        self.cycle(li + 1)
+        be.phase(li, _lib.PHASE_INJ_F, **self._args(li, _lib.PHASE_INJ_F, False))
+        if p.sharded:
+            comm.shift(self.U[li][0], self.U[li][(p.ce - p.cb) * p.m], -1)
+
+    def iteration(self):
+        """One V-cycle, then the fine residual norm^2 (global order) into sumsq."""
+        self.cycle(0)
+        self.comm.allgather(self.partial_all, self.partial)
+        self.be.total(self.partial_all, self.sumsq)
+
+
+def pcg_state_after(seed: int, draws: int):
+    """numpy PCG64 state (state, inc) of default_rng(seed) advanced by `draws` steps."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    state, inc = int(st["state"]), int(st["inc"])
+    M = (2549297995355413924 << 64) | 4865540595714422341
+    mask = (1 << 128) - 1
+    cur_m, cur_p, acc_m, acc_p, d = M, inc, 1, 0, draws
+    while d:
+        if d & 1:
+            acc_m = (acc_m * cur_m) & mask
+            acc_p = (acc_p * cur_m + cur_p) & mask
+        cur_p = ((cur_m + 1) * cur_p) & mask
+        cur_m = (cur_m * cur_m) & mask
+        d >>= 1
+    return (acc_m * state + acc_p) & mask, inc
+
+
+def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: bool = True):
+    """MGRIT solve with the time axis sharded over the ranks of ``comm``.
+
+    Returns (ConvergenceReport, local U rows, LevelPlan of the fine level).
+    Identical iterates and bitwise-identical residual histories for any P.
+    """
+    import time
+    from .core import stream_ptr
+    from .mgrit import ConvergenceReport, _capture, initial_state
+
+    comm = comm or Comm()
+    dev = levels[0].device
+    t0 = time.perf_counter()
+    sizes = [lv.n_steps for lv in levels]
+    factors = [lv.cf for lv in levels[:-1]] + [None]
+    plans = make_plan(sizes, factors, comm.rank, comm.size)
+    p0 = plans[0]
+    n = levels[0].grid.n_points
+    U = torch.empty((p0.local_rows, n), dtype=torch.float64, device=dev)
+    # local rows = global steps row0 .. row0 + local_rows - 1; iterate draws start at global row 1
+    first = p0.row0
+    if first == 0:
+        U[0] = torch.from_numpy(initial_state(cfg, levels[0].grid)).to(dev)
+        rows, start = U[1:], 0
+    else:
+        rows, start = U, (first - 1) * n
+    st, inc = pcg_state_after(cfg.seed, start)
+    m64 = (1 << 64) - 1
+    _lib.check(_lib.load().mgrit_pcg64_fill(st >> 64, st & m64, inc >> 64, inc & m64, rows.numel(),
+                                            int(cfg.iterate == "pm1"), rows.data_ptr(), stream_ptr()), "pcg64")
+    be = CudaPhaseBackend(levels)
+    be.status.zero_()
+    # initial residual over the owned steps (row0+1 .. row0+local_rows-1)
+    nloc = p0.local_rows - 1
+    row_ss = torch.empty(nloc, dtype=torch.float64, device=dev)
+    R = torch.empty((nloc, n), dtype=torch.float64, device=dev)
+    levels[0]._apply(U, p0.row0, 1, nloc, R, U_sub=U[1:], row_sumsq=row_ss)
+    del R
+    row_all = torch.empty(cfg.n_t, dtype=torch.float64, device=dev)
+    comm.allgather(row_all, row_ss)
+    s0 = torch.zeros(1, dtype=torch.float64, device=dev)
+    be.total(row_all, s0)
+    r0 = float(torch.sqrt(s0).item())
+    eng = TimeParallelCycle(plans, n, be, comm, cfg.relaxation, U, dev)
+    hist, state, graph = [r0], "max_iters", None
+    for it in range(cfg.max_iters):
+        if graph is not None:
+            graph.replay()
+        else:
+            eng.iteration()
+            if use_graph and comm.size == 1 and it == 0 and cfg.max_iters > 1:
+                graph = _capture(eng.iteration)
+        r = float(torch.sqrt(eng.sumsq).item())
+        if be.bad():
+            hist.append(float("nan"))
+            state = "diverged"
+            break
+        hist.append(r)
+        if not np.isfinite(r) or r >= cfg.divergence_factor * r0:
+            state = "diverged"
+            break
+        if r <= cfg.rtol * r0:
+            state = "converged"
+            break
+    torch.cuda.synchronize()
+    h = np.array(hist)
+    fac = float(h[-1] / h[-2]) if len(h) > 1 else float("nan")
+    wall = time.perf_counter() - t0
+    return ConvergenceReport(h, len(h) - 1, state, fac, wall, 0.0, wall), U, p0
