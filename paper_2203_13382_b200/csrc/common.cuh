@@ -150,6 +150,16 @@ __device__ __forceinline__ double dcoef<5>(int i) {
     return c[i];
 }
 
+// c_idx * x for the D stencil; the +-1 coefficients are applied exactly
+// without a multiply (1 * x == x, -1 * x == -x in IEEE arithmetic)
+template <int P>
+__device__ __forceinline__ double cmul(int idx, double x) {
+    const double c = dcoef<P>(idx);
+    if (c == 1.0) return x;
+    if (c == -1.0) return -x;
+    return __dmul_rn(c, x);
+}
+
 // ---------------------------------------------------------------------------
 // deterministic reductions
 

@@ -21,6 +21,15 @@
 namespace mgrit {
 
 constexpr int kMaxKrylov = 16;
+
+#ifdef MGRIT_PROBE
+// clock64 timestamps of CTA 0 / thread 0 (tools/probe_gmres.cu only)
+__device__ long long g_probe[512];
+#define MGRIT_PROBE_AT(id) \
+    do { if (threadIdx.x == 0 && blockIdx.x == 0 && (id) < 512) g_probe[(id)] = clock64(); } while (0)
+#else
+#define MGRIT_PROBE_AT(id) do {} while (0)
+#endif
 // periodic halo kept on both sides of the shared-memory row so stencil taps
 // (<= 3 cells: p = 5 interpolation, D_6) need no wrap-around arithmetic
 constexpr int kHalo = 4;
@@ -76,7 +85,11 @@ __device__ __forceinline__ double block_sum2(double v, RowCtx &cx) {
     v = warp_sum(v);
     if (lane == 0) red[warp] = v;
     __syncthreads();
-    return warp_sum(lane < NW ? red[lane] : 0.0);
+    if constexpr (NW <= 8) {
+        return tree_sum<NW>(red);  // few partials: broadcast loads + pairwise tree
+    } else {
+        return warp_sum(lane < NW ? red[lane] : 0.0);
+    }
 }
 
 // a / b with y = RN(1/b): q0 = RN(a y), r = fma(-q0, b, a) (exact),
@@ -112,6 +125,7 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
     const double *row = cx.rowbuf;
 
     // ---- semi-Lagrangian gather: left-to-right sum of rounded products
+    MGRIT_PROBE_AT(0);
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         const int i = tid + k * NT;
@@ -152,14 +166,13 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 acc = 0.0;
 #pragma unroll
                 for (int q = -RAD; q <= RAD; ++q)
-                    acc = __dadd_rn(acc, __dmul_rn(dcoef<P>(RAD + q), row[i + q]));
+                    acc = __dadd_rn(acc, cmul<P>(RAD + q, row[i + q]));
             } else {
                 // coarse_correction.py:50-56: c0 v + sum_k (c_{+k} v_{i+k} + c_{-k} v_{i-k})
-                acc = __dmul_rn(dcoef<P>(RAD), xi);
+                acc = cmul<P>(RAD, xi);
 #pragma unroll
                 for (int q = 1; q <= RAD; ++q)
-                    acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(dcoef<P>(RAD + q), row[i + q]),
-                                                   __dmul_rn(dcoef<P>(RAD - q), row[i - q])));
+                    acc = __dadd_rn(acc, __dadd_rn(cmul<P>(RAD + q, row[i + q]), cmul<P>(RAD - q, row[i - q])));
             }
             double s_i;
             if constexpr (SIGREG) s_i = sg[k];
@@ -184,7 +197,10 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
             return 0;
         } else {
             // ---- MGS-GMRES, zero start, Givens (coarse_correction.py:173-228,
-            //      _kernels.py:34-101) on (I - diag(sig) D) x = v
+            //      _kernels.py:34-101) on (I - diag(sig) D) x = v.
+            // The operator application is the reference's exact arithmetic;
+            // inner products / axpys use FMA (their reference counterparts are
+            // BLAS calls whose rounding is not reproducible anyway).
             const int K = L.gmres_max_iters;
             const double tol = L.gmres_tol;
             GmresSmem &G = *cx.gs;
@@ -200,16 +216,15 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 for (int k = 0; k < NPT; ++k) v[k] = __longlong_as_double(0x7ff8000000000000LL);
                 return -1;
             }
-            auto dot4 = [&](const double *b) -> double {
+            auto sumsq4 = [&]() -> double {
                 double a[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                for (int k = 0; k < NPT; ++k) {
-                    const int i = tid + k * NT;
-                    if (F || i < n) a[k & 3] = __dadd_rn(a[k & 3], __dmul_rn(b ? b[i] : v[k], v[k]));
-                }
+                for (int k = 0; k < NPT; ++k) a[k & 3] = fma(v[k], v[k], a[k & 3]);
                 return __dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3]));
             };
-            const double beta = sqrt(block_sum2<NT>(dot4(nullptr), cx));
+            MGRIT_PROBE_AT(1);
+            const double beta = sqrt(block_sum2<NT>(sumsq4(), cx));
+            MGRIT_PROBE_AT(2);
             if (beta == 0.0) {
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) v[k] = 0.0;
@@ -225,13 +240,11 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                     if (F || i < n) b0[i] = v[k];
                 }
             }
-            if (tid == 0) {
-                G.g[0] = beta;
-                G.stop = 0;
-            }
+            double g_k = beta;  // thread 0: running g[kk] of the least-squares rhs
             int done = 0;
 #pragma unroll 1
             for (int kk = 0; kk < K; ++kk) {
+                MGRIT_PROBE_AT(10 + 8 * kk);
                 __syncthreads();  // previous users of rowbuf are done
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) {
@@ -245,8 +258,12 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                     const int i = tid + k * NT;
                     v[k] = (F || i < n) ? imsd_at(k, i, v[k]) : 0.0;
                 }
+                MGRIT_PROBE_AT(11 + 8 * kk);
                 // modified Gram-Schmidt against b_0..b_kk (b_kk read from rowbuf);
-                // b_{j+1} is fetched into registers while b_j's reduction runs
+                // b_{j+1} is fetched into registers while b_j's reduction runs.
+                // Thread 0 applies the previous Givens rotations to column kk as
+                // its entries arrive (rotation j needs h_j and h_{j+1} only), in
+                // the reference's order.
                 double bc[NPT];
                 {
                     const double *b0p = kk == 0 ? cx.rowbuf : cx.bvec(0, n);
@@ -256,11 +273,12 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                         bc[k] = (F || i < n) ? b0p[i] : 0.0;
                     }
                 }
+                double hrun = 0.0;  // thread 0: column kk entry j after rotations < j
 #pragma unroll 1
                 for (int j = 0; j <= kk; ++j) {
                     double a4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                    for (int k = 0; k < NPT; ++k) a4[k & 3] = __dadd_rn(a4[k & 3], __dmul_rn(bc[k], v[k]));
+                    for (int k = 0; k < NPT; ++k) a4[k & 3] = fma(bc[k], v[k], a4[k & 3]);
                     const double part = __dadd_rn(__dadd_rn(a4[0], a4[1]), __dadd_rn(a4[2], a4[3]));
                     double bn[NPT];
                     if (j < kk) {
@@ -271,68 +289,91 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                             bn[k] = (F || i < n) ? bp[i] : 0.0;
                         }
                     }
+                    double c = 0.0, sn = 0.0;
+                    if (tid == 0 && j > 0) {
+                        c = G.cs[j - 1];
+                        sn = G.sn[j - 1];
+                    }
                     const double h = block_sum2<NT>(part, cx);
-                    if (tid == 0) G.H[j * kMaxKrylov + kk] = h;
+                    if (tid == 0) {
+                        if (j == 0) {
+                            hrun = h;
+                        } else {
+                            // rotation j-1 on rows (j-1, j) of column kk
+                            const double tmp = __dadd_rn(__dmul_rn(c, hrun), __dmul_rn(sn, h));
+                            hrun = __dadd_rn(__dmul_rn(-sn, hrun), __dmul_rn(c, h));
+                            G.H[(j - 1) * kMaxKrylov + kk] = tmp;
+                        }
+                    }
 #pragma unroll
                     for (int k = 0; k < NPT; ++k) {
-                        v[k] = __dsub_rn(v[k], __dmul_rn(h, bc[k]));
+                        v[k] = fma(-h, bc[k], v[k]);
                         bc[k] = bn[k];
                     }
                 }
-                const double nrm = sqrt(block_sum2<NT>(dot4(nullptr), cx));
+                MGRIT_PROBE_AT(12 + 8 * kk);
+                const double nrm = sqrt(block_sum2<NT>(sumsq4(), cx));
+                MGRIT_PROBE_AT(13 + 8 * kk);
                 const bool brk = nrm <= __dmul_rn(1e-14, beta);
                 if (!brk) {
                     const double yn = 1.0 / nrm;
-                    double *bn = cx.bvec(kk + 1, n);
+                    double *bnv = cx.bvec(kk + 1, n);
 #pragma unroll
                     for (int k = 0; k < NPT; ++k) {
                         const int i = tid + k * NT;
                         v[k] = div_rcp(v[k], nrm, yn);
-                        if (F || i < n) bn[i] = v[k];
+                        if (F || i < n) bnv[i] = v[k];
                     }
                 }
+                MGRIT_PROBE_AT(14 + 8 * kk);
                 if (tid == 0) {
-                    double *H = G.H;
-                    auto h_ = [&](int a, int b) -> double & { return H[a * kMaxKrylov + b]; };
-                    h_(kk + 1, kk) = nrm;
-                    for (int j = 0; j < kk; ++j) {
-                        const double tmp = __dadd_rn(__dmul_rn(G.cs[j], h_(j, kk)), __dmul_rn(G.sn[j], h_(j + 1, kk)));
-                        h_(j + 1, kk) = __dadd_rn(__dmul_rn(-G.sn[j], h_(j, kk)), __dmul_rn(G.cs[j], h_(j + 1, kk)));
-                        h_(j, kk) = tmp;
-                    }
-                    const double den = hypot(h_(kk, kk), h_(kk + 1, kk));
-                    G.cs[kk] = __ddiv_rn(h_(kk, kk), den);
-                    G.sn[kk] = __ddiv_rn(h_(kk + 1, kk), den);
-                    h_(kk, kk) = den;
-                    h_(kk + 1, kk) = 0.0;
-                    G.g[kk + 1] = __dmul_rn(-G.sn[kk], G.g[kk]);
-                    G.g[kk] = __dmul_rn(G.cs[kk], G.g[kk]);
-                    G.stop = brk || (tol >= 0.0 && fabs(G.g[kk + 1]) <= __dmul_rn(tol, beta));
-                    if (G.stop || kk + 1 == K) {
-                        // back substitution (_kernels.py:90-95)
-                        const int d = kk + 1;
-                        for (int j = d - 1; j >= 0; --j) {
-                            double acc = G.g[j];
-                            for (int jj = j + 1; jj < d; ++jj)
-                                acc = __dsub_rn(acc, __dmul_rn(h_(j, jj), G.y[jj]));
-                            G.y[j] = __ddiv_rn(acc, h_(j, j));
-                        }
-                    }
+                    // new rotation from (H[kk][kk], h_{kk+1,kk} = nrm)
+                    const double den = hypot(hrun, nrm);
+                    const double c = __ddiv_rn(hrun, den), sn = __ddiv_rn(nrm, den);
+                    G.cs[kk] = c;
+                    G.sn[kk] = sn;
+                    G.H[kk * kMaxKrylov + kk] = den;
+                    const double gn = __dmul_rn(-sn, g_k);
+                    G.g[kk] = __dmul_rn(c, g_k);
+                    G.g[kk + 1] = gn;
+                    g_k = gn;
+                    G.stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta));
                 }
+                MGRIT_PROBE_AT(15 + 8 * kk);
                 done = kk + 1;
                 __syncthreads();
+                MGRIT_PROBE_AT(16 + 8 * kk);
                 if (G.stop) break;
             }
-            // x = sum_j b_j y_j (_kernels.py:96-101)
-#pragma unroll
-            for (int k = 0; k < NPT; ++k) {
-                const int i = tid + k * NT;
-                double acc = 0.0;
-                if (F || i < n)
-                    for (int j = 0; j < done; ++j)
-                        acc = __dadd_rn(acc, __dmul_rn(cx.bvec(j, n)[i], G.y[j]));
-                v[k] = acc;
+            // back substitution on warp 0 (column-oriented, as LAPACK trsv):
+            // lane i keeps acc_i = g_i - sum_{j>i} H[i][j] y_j
+            if (tid < 32) {
+                const int lane = tid;
+                double acc = lane < done ? G.g[lane] : 0.0;
+                for (int j = done - 1; j >= 0; --j) {
+                    double yj = 0.0;
+                    if (lane == j) yj = __ddiv_rn(acc, G.H[j * kMaxKrylov + j]);
+                    yj = __shfl_sync(0xffffffffu, yj, j);
+                    if (lane == j) G.y[j] = yj;
+                    if (lane < j) acc = __dsub_rn(acc, __dmul_rn(G.H[lane * kMaxKrylov + j], yj));
+                }
             }
+            __syncthreads();
+            MGRIT_PROBE_AT(200);
+            // x = sum_j b_j y_j (_kernels.py:96-101), j ascending per node
+#pragma unroll
+            for (int k = 0; k < NPT; ++k) v[k] = 0.0;
+#pragma unroll 1
+            for (int j = 0; j < done; ++j) {
+                const double yj = G.y[j];
+                const double *bj = cx.bvec(j, n);
+#pragma unroll
+                for (int k = 0; k < NPT; ++k) {
+                    const int i = tid + k * NT;
+                    if (F || i < n) v[k] = fma(bj[i], yj, v[k]);
+                }
+            }
+            MGRIT_PROBE_AT(201);
             return done;
         }
     }
