@@ -138,7 +138,8 @@ int mgrit_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
  *   S_b   = Phi_{t_b} U_in[b]          (t_b = t_idx ? t_idx[b] : t_first + b*t_stride)
  *   relax form    (U_sub == NULL): out[b] = S_b + G[b]           (G NULL => + 0.0)
  *   residual form (U_sub != NULL): out[b] = (G[b] + S_b) - U_sub[b]
- * row_sumsq (nullable, [B]): sum of out[b]^2 per row (fixed order).
+ * row_sumsq (nullable, [B]): sum of out[b]^2 per row (fixed order);
+ *   out may be NULL when row_sumsq is given (norms only, no rows written).
  * gmres_iters (nullable, [B]): Arnoldi steps per corrected row.
  * scratch: >= mgrit_gmres_scratch_bytes(L, B) bytes for corrected levels. */
 int mgrit_apply_rows(const mgrit_level_desc *L, int64_t B, const int64_t *t_idx,

@@ -71,7 +71,7 @@ extern "C" int mgrit_apply_rows(const mgrit_level_desc *L, int64_t B, const int6
                                 int64_t ld_sub, double *out, int64_t ld_out, double *row_sumsq,
                                 int32_t *gmres_iters, void *scratch, int64_t scratch_bytes,
                                 int32_t *status, void *stream) {
-    if (!L || B < 0 || (B > 0 && (!U_in || !out)) || !status) return MGRIT_EINVAL;
+    if (!L || B < 0 || (B > 0 && (!U_in || (!out && !row_sumsq))) || !status) return MGRIT_EINVAL;
     RowsArgs a{B, t_idx, t_first, t_stride, U_in, ld_in, G, ld_g, U_sub, ld_sub, out, ld_out,
                row_sumsq, gmres_iters};
     if (L->dim == 1) return apply_rows_1d(L, a, scratch, scratch_bytes, status, (cudaStream_t)stream);

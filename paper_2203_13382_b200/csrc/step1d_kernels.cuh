@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(NT) rows_kernel(mgrit_level_desc L, RowsArgs a
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) ss = __dadd_rn(ss, __dmul_rn(v[k], v[k]));
         }
-        store_row<NT, NPT, F>(a.out + b * a.ld_out, v, n);
+        if (a.out) store_row<NT, NPT, F>(a.out + b * a.ld_out, v, n);
         if (a.row_sumsq) {
             const double tot = block_sum2<NT>(ss, cx);
             if (threadIdx.x == 0) a.row_sumsq[b] = tot;

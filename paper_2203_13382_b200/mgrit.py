@@ -223,7 +223,7 @@ class Level:
         rc = lib.mgrit_apply_rows(
             ctypes.byref(d), B, _ptr(t_idx), t_first, t_stride,
             U_in.data_ptr(), ld_in or n, _ptr(G), ld_g or n, _ptr(U_sub), ld_sub or n,
-            out.data_ptr(), ld_out or n, _ptr(row_sumsq), _ptr(gmres_iters), _ptr(scr),
+            _ptr(out), ld_out or n, _ptr(row_sumsq), _ptr(gmres_iters), _ptr(scr),
             0 if scr is None else scr.numel(), _WS.get_status(dev).data_ptr(), stream_ptr())
         _lib.check(rc, "apply_rows")
 
@@ -651,7 +651,11 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
     fine = levels[0]
     grid = fine.grid
     n = grid.n_points
-    U = torch.empty((cfg.n_t + 1, n), dtype=torch.float64, device=dev)
+    use_fused = (engine == "fused") or (engine == "auto" and _fused_ok(levels))
+    if use_fused and not _fused_ok(levels):
+        raise ValueError("fused engine supports 1D non-ideal hierarchies")
+    sess = _session(levels, cfg, dev) if use_fused else None
+    U = sess.U if sess is not None else torch.empty((cfg.n_t + 1, n), dtype=torch.float64, device=dev)
     U[0] = torch.from_numpy(initial_state(cfg, grid)).to(dev)
     if initial_iterate is not None:
         src = torch.as_tensor(initial_iterate)
@@ -660,30 +664,25 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
         pcg64_uniform(cfg.seed, cfg.n_t, n, U[1:], pm1=(cfg.iterate == "pm1"))
     status = _WS.get_status(dev)
     status.zero_()
-    use_fused = (engine == "fused") or (engine == "auto" and _fused_ok(levels))
-    if use_fused and not _fused_ok(levels):
-        raise ValueError("fused engine supports 1D non-ideal hierarchies")
 
-    # initial residual r0 (all rows: the random iterate has F-point residuals)
-    row_ss = torch.empty(cfg.n_t, dtype=torch.float64, device=dev)
-    R = torch.empty((cfg.n_t, n), dtype=torch.float64, device=dev)
-    fine._apply(U, 0, 1, cfg.n_t, R, U_sub=U[1:], row_sumsq=row_ss)
+    # initial residual r0 (all rows: the random iterate has F-point residuals);
+    # only the per-row sums of squares are produced (no residual array)
+    row_ss = sess.row_ss if sess is not None else torch.empty(cfg.n_t, dtype=torch.float64, device=dev)
+    fine._apply(U, 0, 1, cfg.n_t, None, U_sub=U[1:], row_sumsq=row_ss)
     r0 = float(torch.sqrt(device_sum(row_ss)).item())
-    del R
     history = [r0]
     state = "max_iters"
     G0 = torch.zeros_like(U) if not use_fused else None
 
     if use_fused:
-        eng = _FusedCycle(levels, U, cfg.relaxation)
-        graph = None
+        eng = sess.engine
         for it in range(cfg.max_iters):
-            if graph is not None:
-                graph.replay()
+            if sess.graph is not None and use_graph:
+                sess.graph.replay()
             else:
                 eng.iteration()
-                if use_graph and it == 0 and cfg.max_iters > 1:
-                    graph = _capture(eng.iteration)
+                if use_graph and cfg.max_iters > 1:
+                    sess.graph = _capture(eng.iteration)
             ss = float(eng.sumsq.item())
             bad = int(status.item())
             if bad:
@@ -719,14 +718,40 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
         dst = torch.from_numpy(out) if isinstance(out, np.ndarray) else out
         dst.copy_(U)
         result = dst.numpy()
+    elif output == "numpy":
+        result = U.cpu().numpy()
     else:
-        result = U.cpu().numpy() if output == "numpy" else U
+        result = U.clone() if sess is not None else U
     torch.cuda.synchronize()
     t_end = time.perf_counter()
     hist = np.array(history)
     factor = float(hist[-1] / hist[-2]) if len(hist) > 1 else float("nan")
     rep = ConvergenceReport(hist, len(hist) - 1, state, factor, t_end - t_begin, t_setup, t_end - t_solve0)
     return rep, result
+
+
+@dataclass
+class _Session:
+    """Per-hierarchy solve workspace: the state buffer, the fused engine and
+    its captured CUDA graph survive across solve() calls on the same levels."""
+
+    U: torch.Tensor
+    row_ss: torch.Tensor
+    engine: "_FusedCycle"
+    graph: object = None
+
+
+def _session(levels, cfg, dev) -> _Session:
+    key = (cfg.n_t, cfg.relaxation, tuple((lv.kind, lv.gmres_cfg, lv.stencil_numba) for lv in levels))
+    cache = levels[0].__dict__.setdefault("_sessions", {})
+    sess = cache.get(key)
+    if sess is None:
+        n = levels[0].grid.n_points
+        U = torch.empty((cfg.n_t + 1, n), dtype=torch.float64, device=dev)
+        sess = _Session(U, torch.empty(cfg.n_t, dtype=torch.float64, device=dev),
+                        _FusedCycle(levels, U, cfg.relaxation))
+        cache[key] = sess
+    return sess
 
 
 def _capture(fn):

@@ -262,9 +262,23 @@ def pcg_state_after(seed: int, draws: int):
     return (acc_m * state + acc_p) & mask, inc
 
 
-def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: bool = True):
+def local_rows(cfg, levels, comm: Comm | None = None) -> tuple[int, int]:
+    """(first global step, row count) of this rank's fine-level state rows."""
+    comm = comm or Comm()
+    sizes = [lv.n_steps for lv in levels]
+    factors = [lv.cf for lv in levels[:-1]] + [None]
+    p0 = make_plan(sizes, factors, comm.rank, comm.size)[0]
+    return p0.row0, p0.local_rows
+
+
+def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: bool = True,
+                        iterate0=None, out=None):
     """MGRIT solve with the time axis sharded over the ranks of ``comm``.
 
+    ``iterate0``: optional host tensor with this rank's initial-iterate rows
+    (global steps max(row0, 1) .. row0 + local_rows - 1); default: numpy's
+    PCG64 stream generated on the device from the matching offset.
+    ``out``: optional host tensor (local_rows, n_points) receiving the rows.
     Returns (ConvergenceReport, local U rows, LevelPlan of the fine level).
     Identical iterates and bitwise-identical residual histories for any P.
     """
@@ -288,10 +302,14 @@ def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: boo
         rows, start = U[1:], 0
     else:
         rows, start = U, (first - 1) * n
-    st, inc = pcg_state_after(cfg.seed, start)
-    m64 = (1 << 64) - 1
-    _lib.check(_lib.load().mgrit_pcg64_fill(st >> 64, st & m64, inc >> 64, inc & m64, rows.numel(),
-                                            int(cfg.iterate == "pm1"), rows.data_ptr(), stream_ptr()), "pcg64")
+    if iterate0 is not None:
+        rows.copy_(torch.as_tensor(iterate0).reshape(rows.shape), non_blocking=True)
+    else:
+        st, inc = pcg_state_after(cfg.seed, start)
+        m64 = (1 << 64) - 1
+        _lib.check(_lib.load().mgrit_pcg64_fill(st >> 64, st & m64, inc >> 64, inc & m64, rows.numel(),
+                                                int(cfg.iterate == "pm1"), rows.data_ptr(), stream_ptr()),
+                   "pcg64")
     be = CudaPhaseBackend(levels)
     be.status.zero_()
     # initial residual over the owned steps (row0+1 .. row0+local_rows-1)
@@ -326,6 +344,8 @@ def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: boo
         if r <= cfg.rtol * r0:
             state = "converged"
             break
+    if out is not None:
+        out.copy_(U)
     torch.cuda.synchronize()
     h = np.array(hist)
     fac = float(h[-1] / h[-2]) if len(h) > 1 else float("nan")

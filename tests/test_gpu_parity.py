@@ -340,3 +340,19 @@ def test_non_finite_iterate_status_matches_oracle(P, row):
     assert rep.status == orep.status
     assert rep.iterations == orep.iterations
     assert np.array_equal(np.isfinite(rep.residual_norms), np.isfinite(orep.residual_norms))
+
+
+def test_time_parallel_engine_single_rank_equals_fused(P):
+    """timepar.solve_time_parallel (the multi-GPU engine) with one rank is
+    bit-identical to the single-GPU fused solve: same iterates, same norms."""
+    from paper_2203_13382_b200 import timepar as T
+    for kw in (dict(n_x=128, n_t=256, wave_speed="B2", p=3, schedule=4, seed=1),
+               dict(n_x=64, n_t=128, wave_speed="C3", p=1, schedule=4, relaxation="F")):
+        cfg = P.SolverConfig(**kw)
+        levels = P.build_hierarchy(cfg)
+        r1, U1 = P.solve(cfg, levels)
+        r2, U2, p0 = T.solve_time_parallel(cfg, levels)
+        assert (p0.row0, p0.local_rows) == (0, cfg.n_t + 1)
+        assert np.array_equal(U1, _np(U2))
+        assert np.array_equal(r1.residual_norms, r2.residual_norms)
+        assert r1.status == r2.status
