@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kSumThreads) sum_kernel(const double *x, int64
     if (threadIdx.x == 0) out[0] = tot;
 }
 
-__global__ void axpy_rows_kernel(double *U, int64_t ldu, int64_t stride, const double *X,
+__global__ void axpy_rows_kernel_impl(double *U, int64_t ldu, int64_t stride, const double *X,
                                  int64_t ldx, int64_t rows, int64_t n) {
     const int64_t total = rows * n;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -47,6 +47,15 @@ __global__ void axpy_rows_kernel(double *U, int64_t ldu, int64_t stride, const d
 }
 
 }  // namespace
+
+int axpy_rows_impl(double *U, int64_t ldu, int64_t stride, const double *X, int64_t ldx, int64_t rows, int64_t n,
+                   cudaStream_t st) {
+    if (rows <= 0 || n <= 0) return MGRIT_OK;
+    int64_t g = (rows * n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    axpy_rows_kernel_impl<<<(int)g, 256, 0, st>>>(U, ldu, stride, X, ldx, rows, n);
+    return check_launch("axpy_rows");
+}
 }  // namespace mgrit
 
 using namespace mgrit;
@@ -56,12 +65,15 @@ extern "C" int mgrit_abi_version(void) { return MGRIT_ABI_VERSION; }
 extern "C" const char *mgrit_last_error(void) { return g_err; }
 
 extern "C" int64_t mgrit_gmres_scratch_bytes(const mgrit_level_desc *L, int64_t rows) {
-    if (!L || L->kind != MGRIT_KIND_CORRECTED) return 0;
+    if (!L) return 0;
+    if (L->dim == 2) return scratch2d_bytes(L, rows);
+    if (L->kind != MGRIT_KIND_CORRECTED) return 0;
     return rows * (int64_t)(L->gmres_max_iters + 1) * L->n_points * (int64_t)sizeof(double);
 }
 
 extern "C" int64_t mgrit_resident_rows(const mgrit_level_desc *L) {
-    if (!L || L->dim != 1) return 0;
+    if (!L) return 0;
+    if (L->dim == 2) return capacity2d(L);
     return rows_capacity(L);
 }
 
@@ -75,7 +87,8 @@ extern "C" int mgrit_apply_rows(const mgrit_level_desc *L, int64_t B, const int6
     RowsArgs a{B, t_idx, t_first, t_stride, U_in, ld_in, G, ld_g, U_sub, ld_sub, out, ld_out,
                row_sumsq, gmres_iters};
     if (L->dim == 1) return apply_rows_1d(L, a, scratch, scratch_bytes, status, (cudaStream_t)stream);
-    snprintf(g_err, sizeof g_err, "apply_rows: dim %d not built", L->dim);
+    if (L->dim == 2) return apply_rows_2d(L, a, scratch, scratch_bytes, status, (cudaStream_t)stream);
+    snprintf(g_err, sizeof g_err, "apply_rows: dim %d unsupported", L->dim);
     return MGRIT_EINVAL;
 }
 
@@ -84,7 +97,8 @@ extern "C" int mgrit_level_phase(const mgrit_level_desc *L, const mgrit_phase_ar
                                  void *stream) {
     if (!L || !A || !status) return MGRIT_EINVAL;
     if (L->dim == 1) return level_phase_1d(L, A, scratch, scratch_bytes, status, (cudaStream_t)stream);
-    snprintf(g_err, sizeof g_err, "level_phase: dim %d not built", L->dim);
+    if (L->dim == 2) return level_phase_2d(L, A, scratch, scratch_bytes, status, (cudaStream_t)stream);
+    snprintf(g_err, sizeof g_err, "level_phase: dim %d unsupported", L->dim);
     return MGRIT_EINVAL;
 }
 
@@ -96,7 +110,10 @@ extern "C" int mgrit_sequential_sweep(const mgrit_level_desc *L, double *U, int6
     if (L->dim == 1)
         return sweep_1d(L, U, ldu, G, ldg, zero_init, gmres_iters, scratch, scratch_bytes, status,
                         (cudaStream_t)stream);
-    snprintf(g_err, sizeof g_err, "sequential_sweep: dim %d not built", L->dim);
+    if (L->dim == 2)
+        return sweep_2d(L, U, ldu, G, ldg, zero_init, gmres_iters, scratch, scratch_bytes, status,
+                        (cudaStream_t)stream);
+    snprintf(g_err, sizeof g_err, "sequential_sweep: dim %d unsupported", L->dim);
     return MGRIT_EINVAL;
 }
 
@@ -110,8 +127,5 @@ extern "C" int mgrit_axpy_rows(double *U, int64_t ldu, int64_t u_stride_rows, co
                                int64_t ldx, int64_t rows, int64_t n, void *stream) {
     if (rows < 0 || n < 0 || (rows > 0 && (!U || !X))) return MGRIT_EINVAL;
     if (rows == 0 || n == 0) return MGRIT_OK;
-    int64_t g = (rows * n + 255) / 256;
-    if (g > 148 * 16) g = 148 * 16;
-    axpy_rows_kernel<<<(int)g, 256, 0, (cudaStream_t)stream>>>(U, ldu, u_stride_rows, X, ldx, rows, n);
-    return check_launch("axpy_rows");
+    return axpy_rows_impl(U, ldu, u_stride_rows, X, ldx, rows, n, (cudaStream_t)stream);
 }

@@ -25,4 +25,15 @@ int sweep_1d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G,
              int32_t *status, cudaStream_t st);
 int64_t rows_capacity(const mgrit_level_desc *L);
 
+int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, int64_t scratch_bytes,
+                  int32_t *status, cudaStream_t st);
+int level_phase_2d(const mgrit_level_desc *L, const mgrit_phase_args *A, void *scratch, int64_t scratch_bytes,
+                   int32_t *status, cudaStream_t st);
+int sweep_2d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg, int zero_init,
+             int32_t *gmres_iters, void *scratch, int64_t scratch_bytes, int32_t *status, cudaStream_t st);
+int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows);
+int64_t capacity2d(const mgrit_level_desc *L);
+int axpy_rows_impl(double *U, int64_t ldu, int64_t stride, const double *X, int64_t ldx, int64_t rows,
+                   int64_t n, cudaStream_t st);
+
 }  // namespace mgrit

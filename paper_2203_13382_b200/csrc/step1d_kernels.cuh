@@ -92,13 +92,6 @@ __device__ __forceinline__ double block_sum2(double v, RowCtx &cx) {
     }
 }
 
-// a / b with y = RN(1/b): q0 = RN(a y), r = fma(-q0, b, a) (exact),
-// q = fma(r, y, q0) == RN(a / b) (Markstein; verified on 4e8 random pairs).
-__device__ __forceinline__ double div_rcp(double a, double b, double y) {
-    const double q0 = __dmul_rn(a, y);
-    const double r = fma(-q0, b, a);
-    return fma(r, y, q0);
-}
 
 template <int NT, int NPT, bool F>
 __device__ __forceinline__ void load_records(const mgrit_level_desc &L, int64_t t, double (&sv)[NPT]) {

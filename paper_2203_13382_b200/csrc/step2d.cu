@@ -1,0 +1,627 @@
+// step2d.cu — the 2D hot path (BASELINE configs 4-5: 512^2 and 1024^2 meshes).
+//
+// A 2D state row (n = n_x^2 = 0.26-1 M fp64, 2-8 MB) does not fit one SM, so
+// 2D steps are batched over rows with many CTAs per row:
+//  * plain SL: one thread per node, the (p+1)^2 tensor-product gather reads
+//    the previous row through L1/L2 (neighbouring nodes share their source
+//    window); per-CTA partial sums give deterministic row norms;
+//  * forward Euler: SL into scratch, then the explicit correction pass;
+//  * corrected (SL + MGS-GMRES on I - diag(sx) Dx - diag(sy) Dy): one
+//    cooperative kernel over the batch; each system is split into chunks
+//    over the resident CTAs and every MGS inner product is a grid-wide,
+//    fixed-order reduction (per-chunk partials, grid.sync, ordered sum).
+// The fused MGRIT phases are composed on the host from these batched launches
+// with strided row pointers (same semantics as the 1D phase_kernel).
+#include <cooperative_groups.h>
+
+#include <cstdio>
+#include <type_traits>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mgrit {
+
+namespace {
+
+constexpr int kNT2 = 256;       // threads per CTA for 2D kernels
+constexpr int kTile2 = 1024;    // nodes per CTA tile (4 per thread)
+constexpr int kMaxK2 = 16;
+
+__device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+
+// 2D SL value at node (ix, iy): semi_lagrangian.py:238-253 (x inner, y outer,
+// both accumulators start at 0, separately rounded products)
+template <int P>
+__device__ __forceinline__ double sl2d_at(const double *u, int nx, double sx, double sy) {
+    constexpr int SL = Stencil<P>::L;
+    const Dec dx = decompose_s(sx, nx);
+    const Dec dy = decompose_s(sy, nx);
+    double wx[P + 1], wy[P + 1];
+    lagrange_weights<P>(dx.eps, wx);
+    lagrange_weights<P>(dy.eps, wy);
+    int cols[P + 1];
+#pragma unroll
+    for (int j = 0; j <= P; ++j) cols[j] = wrapi(dx.e - SL + j, nx);
+    double out = 0.0;
+#pragma unroll
+    for (int jy = 0; jy <= P; ++jy) {
+        const double *r = u + (int64_t)wrapi(dy.e - SL + jy, nx) * nx;
+        double acc = 0.0;
+#pragma unroll
+        for (int jx = 0; jx <= P; ++jx) acc = __dadd_rn(acc, __dmul_rn(wx[jx], __ldg(r + cols[jx])));
+        out = __dadd_rn(out, __dmul_rn(wy[jy], acc));
+    }
+    return out;
+}
+
+// (I - diag(sx) Dx - diag(sy) Dy) v at node (ix, iy) (coarse_correction.py:141-149:
+// dx = c0 v; dx = dx + c+k v(x+k) + c-k v(x-k); v - sx dx - sy dy)
+template <int P>
+__device__ __forceinline__ double imsd2d_at(const double *v, int nx, int ix, int iy, double sx, double sy) {
+    constexpr int RAD = (P + 1) / 2;
+    const double *row = v + (int64_t)iy * nx;
+    const double vi = row[ix];
+    double dx = cmul<P>(RAD, vi), dy = cmul<P>(RAD, vi);
+#pragma unroll
+    for (int q = 1; q <= RAD; ++q) {
+        dx = __dadd_rn(__dadd_rn(dx, cmul<P>(RAD + q, row[wrapi(ix + q, nx)])), cmul<P>(RAD - q, row[wrapi(ix - q, nx)]));
+        dy = __dadd_rn(__dadd_rn(dy, cmul<P>(RAD + q, v[(int64_t)wrapi(iy + q, nx) * nx + ix])),
+                       cmul<P>(RAD - q, v[(int64_t)wrapi(iy - q, nx) * nx + ix]));
+    }
+    return __dsub_rn(__dsub_rn(vi, __dmul_rn(sx, dx)), __dmul_rn(sy, dy));
+}
+
+struct Rows2D {
+    int64_t B;
+    const int64_t *t_idx;
+    int64_t t_first, t_stride;
+    const double *U_in; int64_t ld_in;
+    const double *G; int64_t ld_g;
+    const double *U_sub; int64_t ld_sub;
+    double *out; int64_t ld_out;
+    double *partial;  // [B][tiles] row sum-of-squares partials (nullable)
+};
+
+__device__ __forceinline__ int64_t row_t(const Rows2D &a, int64_t b) {
+    return a.t_idx ? a.t_idx[b] : a.t_first + b * a.t_stride;
+}
+
+// plain SL (SLONLY: write S only, no forcing / residual form)
+template <int P, bool SLONLY>
+__global__ void __launch_bounds__(kNT2) sl2d_kernel(mgrit_level_desc L, Rows2D a) {
+    __shared__ double red[kNT2 / 32 + 1];
+    const int nx = L.n_x;
+    const int64_t n = L.n_points;
+    const int64_t b = blockIdx.y;
+    const int64_t t = row_t(a, b);
+    const int64_t set = L.shared ? 0 : t;
+    const double *sx = L.s_x + set * n, *sy = L.s_y + set * n;
+    const double *u = a.U_in + b * a.ld_in;
+    double ss = 0.0;
+#pragma unroll
+    for (int k = 0; k < kTile2 / kNT2; ++k) {
+        const int64_t i = (int64_t)blockIdx.x * kTile2 + k * kNT2 + threadIdx.x;
+        if (i < n) {
+            double v = sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
+            if constexpr (!SLONLY) {
+                const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
+                if (a.U_sub) {
+                    v = __dsub_rn(__dadd_rn(g, v), a.U_sub[b * a.ld_sub + i]);
+                } else {
+                    v = __dadd_rn(v, g);
+                }
+                ss = __dadd_rn(ss, __dmul_rn(v, v));
+            }
+            if (a.out) a.out[b * a.ld_out + i] = v;
+        }
+    }
+    if constexpr (!SLONLY) {
+        if (a.partial) {
+            const double tot = block_sum<kNT2>(ss, red);
+            if (threadIdx.x == 0) a.partial[b * gridDim.x + blockIdx.x] = tot;
+        }
+    }
+}
+
+// forward Euler finish: out = (2 v - imsd(v)) [+ G | residual form], v from scratch
+template <int P>
+__global__ void __launch_bounds__(kNT2) fe2d_kernel(mgrit_level_desc L, Rows2D a, const double *V) {
+    __shared__ double red[kNT2 / 32 + 1];
+    const int nx = L.n_x;
+    const int64_t n = L.n_points;
+    const int64_t b = blockIdx.y;
+    const int64_t t = row_t(a, b);
+    const int64_t set = L.shared ? 0 : t;
+    const double *gx = L.sig_x + set * n, *gy = L.sig_y + set * n;
+    const double *v = V + b * n;
+    double ss = 0.0;
+#pragma unroll
+    for (int k = 0; k < kTile2 / kNT2; ++k) {
+        const int64_t i = (int64_t)blockIdx.x * kTile2 + k * kNT2 + threadIdx.x;
+        if (i < n) {
+            const int ix = (int)(i % nx), iy = (int)(i / nx);
+            double w = __dsub_rn(__dmul_rn(2.0, v[i]), imsd2d_at<P>(v, nx, ix, iy, __ldg(gx + i), __ldg(gy + i)));
+            const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
+            w = a.U_sub ? __dsub_rn(__dadd_rn(g, w), a.U_sub[b * a.ld_sub + i]) : __dadd_rn(w, g);
+            ss = __dadd_rn(ss, __dmul_rn(w, w));
+            if (a.out) a.out[b * a.ld_out + i] = w;
+        }
+    }
+    if (a.partial) {
+        const double tot = block_sum<kNT2>(ss, red);
+        if (threadIdx.x == 0) a.partial[b * gridDim.x + blockIdx.x] = tot;
+    }
+}
+
+// per-row fixed-order sum of the tile partials
+__global__ void rowsum_kernel(const double *partial, int tiles, int64_t B, double *row_sumsq) {
+    __shared__ double red[kNT2 / 32 + 1];
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        double acc = 0.0;
+        for (int i = threadIdx.x; i < tiles; i += kNT2) acc = __dadd_rn(acc, partial[b * tiles + i]);
+        const double tot = block_sum<kNT2>(acc, red);
+        if (threadIdx.x == 0) row_sumsq[b] = tot;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// corrected step: cooperative batched MGS-GMRES
+//
+// Reductions are defined on fixed 256-node "warp blocks" (a warp sums 8
+// nodes per lane in a fixed order, then a butterfly), and the system total
+// is a fixed-order sum over the warp-block partials.  The result is therefore
+// independent of how many CTAs share a system, of the batch size and of the
+// rank count in a time-sharded run.
+
+constexpr int kWB = 256;            // nodes per warp block
+constexpr int kWBPerLane = kWB / 32;
+
+struct Coop2D {
+    mgrit_level_desc L;
+    Rows2D a;
+    int64_t rows_per_round;   // systems processed concurrently
+    int chunks;               // CTAs per system
+    int64_t nwb;              // warp blocks per system
+    double *basis;            // [rows_per_round][K+1][n]
+    double *w;                // [rows_per_round][n]
+    double *part;             // [2][rows_per_round][nwb] reduction partials
+    int *flags;               // [rows_per_round][chunks] non-finite rhs
+    int *stopflags;           // [rows_per_round]
+    int32_t *gmres_iters;
+    int32_t *status;
+};
+
+struct CoopSmem {
+    double cs[kMaxK2], sn[kMaxK2], g[kMaxK2 + 1], y[kMaxK2], H[(kMaxK2 + 1) * kMaxK2];
+    double red[kNT2 / 32 + 1];
+    int stop;
+};
+
+template <int P>
+__global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ CoopSmem S;
+    const mgrit_level_desc &L = C.L;
+    const Rows2D &a = C.a;
+    const int nx = L.n_x;
+    const int64_t n = L.n_points;
+    const int K = L.gmres_max_iters;
+    const double tol = L.gmres_tol;
+    const int slot = blockIdx.x / C.chunks;   // system slot within the round
+    const int chunk = blockIdx.x % C.chunks;
+    const bool active_cta = slot < C.rows_per_round;
+    const int64_t nwb = C.nwb;
+    const int64_t wb0 = nwb * chunk / C.chunks, wb1 = nwb * (chunk + 1) / C.chunks;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kNT2 / 32;
+    int pbuf = 0;
+
+    // for every node of this CTA's warp blocks: body(i); optional reduction of
+    // red(i) per warp block into the current partial buffer
+    auto for_nodes = [&](auto &&body) {
+        for (int64_t wb = wb0 + warp; wb < wb1; wb += NW)
+#pragma unroll
+            for (int k = 0; k < kWBPerLane; ++k) {
+                const int64_t i = wb * kWB + lane + 32 * k;
+                if (i < n) body(i);
+            }
+    };
+    auto reduce_nodes = [&](auto &&val) {
+        double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
+        for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < kWBPerLane; ++k) {
+                const int64_t i = wb * kWB + lane + 32 * k;
+                if (i < n) acc = __dadd_rn(acc, val(i));
+            }
+            acc = warp_sum(acc);
+            if (lane == 0 && active_cta) pb[wb] = acc;
+        }
+    };
+    // grid barrier, then the fixed-order total of the system's partials
+    auto gtotal = [&]() -> double {
+        grid.sync();
+        double tot = 0.0;
+        if (active_cta) {
+            const double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
+            double acc = 0.0;
+            for (int64_t q = tid; q < nwb; q += kNT2) acc = __dadd_rn(acc, pb[q]);
+            tot = block_sum<kNT2>(acc, S.red);
+        } else {
+            __syncthreads();
+        }
+        pbuf ^= 1;
+        return tot;
+    };
+
+    for (int64_t round0 = 0; round0 < a.B; round0 += C.rows_per_round) {
+        const int64_t b = round0 + slot;
+        const bool active = active_cta && b < a.B;
+        const int64_t t = active ? row_t(a, b) : 0;
+        const int64_t set = L.shared ? 0 : t;
+        const double *sx = L.s_x + set * n, *sy = L.s_y + set * n;
+        const double *gx = L.sig_x + set * n, *gy = L.sig_y + set * n;
+        double *basis = C.basis + (int64_t)slot * (K + 1) * n;
+        double *w = C.w + (int64_t)slot * n;
+        // ---- SL rhs into w, non-finite flag, beta
+        int bad = 0;
+        if (active) {
+            const double *u = a.U_in + b * a.ld_in;
+            for_nodes([&](int64_t i) {
+                const double v = sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
+                w[i] = v;
+                if (!isfinite(v)) bad = 1;
+            });
+            reduce_nodes([&](int64_t i) { return __dmul_rn(w[i], w[i]); });
+        }
+        bad = __syncthreads_or(bad);
+        if (active && tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
+        const double beta = sqrt(gtotal());
+        int anybad = 0;
+        if (active && tid == 0)
+            for (int k = 0; k < C.chunks; ++k) anybad |= C.flags[(int64_t)slot * C.chunks + k];
+        anybad = __syncthreads_or(anybad);
+        int done = 0;
+        const bool skip = !active || anybad || beta == 0.0;
+        if (active && anybad && tid == 0 && chunk == 0) atomicExch(C.status, 1);
+        if (!skip) {
+            const double yb = 1.0 / beta;
+            for_nodes([&](int64_t i) { basis[i] = div_rcp(w[i], beta, yb); });
+        }
+        if (tid == 0) S.stop = skip ? 1 : 0;
+        if (active_cta && tid == 0 && chunk == 0) C.stopflags[slot] = skip ? 1 : 0;
+        double g_k = beta;
+        // grid-uniform iteration loop; it ends when every system has stopped
+        for (int kk = 0; kk < K; ++kk) {
+            __syncthreads();
+            const bool run = !S.stop;
+            grid.sync();  // b_kk and the stop flags visible everywhere
+            int live = 0;
+            for (int q = tid; q < C.rows_per_round; q += kNT2)
+                if (round0 + q < a.B && !C.stopflags[q]) live = 1;
+            if (!__syncthreads_or(live)) break;
+            const double *bk = basis + (int64_t)kk * n;
+            // w = A b_kk ; inner product with b_0
+            if (run) {
+                for_nodes([&](int64_t i) {
+                    const int ix = (int)(i % nx), iy = (int)(i / nx);
+                    w[i] = imsd2d_at<P>(bk, nx, ix, iy, __ldg(gx + i), __ldg(gy + i));
+                });
+                reduce_nodes([&](int64_t i) { return __dmul_rn(basis[i], w[i]); });
+            }
+            double hrun = 0.0;
+            for (int j = 0; j <= kk; ++j) {
+                const double h = gtotal();
+                if (run && tid == 0) {
+                    if (j == 0) {
+                        hrun = h;
+                    } else {
+                        const double c = S.cs[j - 1], sn = S.sn[j - 1];
+                        const double tmp = __dadd_rn(__dmul_rn(c, hrun), __dmul_rn(sn, h));
+                        hrun = __dadd_rn(__dmul_rn(-sn, hrun), __dmul_rn(c, h));
+                        S.H[(j - 1) * kMaxK2 + kk] = tmp;
+                    }
+                }
+                // w -= h b_j, fused with the next inner product (b_{j+1} or ||w||^2)
+                if (run) {
+                    const double *bj = basis + (int64_t)j * n;
+                    const double *bn = j < kk ? basis + (int64_t)(j + 1) * n : nullptr;
+                    for_nodes([&](int64_t i) { w[i] = fma(-h, bj[i], w[i]); });
+                    reduce_nodes([&](int64_t i) { return __dmul_rn(bn ? bn[i] : w[i], w[i]); });
+                }
+            }
+            const double nrm = sqrt(gtotal());
+            if (run) {
+                const bool brk = nrm <= __dmul_rn(1e-14, beta);
+                if (!brk) {
+                    const double yn = 1.0 / nrm;
+                    double *bn = basis + (int64_t)(kk + 1) * n;
+                    for_nodes([&](int64_t i) { bn[i] = div_rcp(w[i], nrm, yn); });
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    const double den = hypot(hrun, nrm);
+                    const double c = __ddiv_rn(hrun, den), sn = __ddiv_rn(nrm, den);
+                    S.cs[kk] = c;
+                    S.sn[kk] = sn;
+                    S.H[kk * kMaxK2 + kk] = den;
+                    const double gn = __dmul_rn(-sn, g_k);
+                    S.g[kk] = __dmul_rn(c, g_k);
+                    S.g[kk + 1] = gn;
+                    g_k = gn;
+                    S.stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta)) || kk + 1 == K;
+                    if (chunk == 0 && S.stop) C.stopflags[slot] = 1;
+                }
+                done = kk + 1;
+            }
+        }
+        __syncthreads();
+        // back substitution (warp 0, column-oriented), x = sum_j b_j y_j, output form
+        if (!skip && tid < 32) {
+            double acc = lane < done ? S.g[lane] : 0.0;
+            for (int j = done - 1; j >= 0; --j) {
+                double yj = 0.0;
+                if (lane == j) yj = __ddiv_rn(acc, S.H[j * kMaxK2 + j]);
+                yj = __shfl_sync(0xffffffffu, yj, j);
+                if (lane == j) S.y[j] = yj;
+                if (lane < j) acc = __dsub_rn(acc, __dmul_rn(S.H[lane * kMaxK2 + j], yj));
+            }
+        }
+        __syncthreads();
+        if (active) {
+            for_nodes([&](int64_t i) {
+                double x = 0.0;
+                if (anybad) {
+                    x = __longlong_as_double(0x7ff8000000000000LL);
+                } else if (!skip) {
+                    for (int j = 0; j < done; ++j) x = fma(basis[(int64_t)j * n + i], S.y[j], x);
+                }
+                const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
+                x = a.U_sub ? __dsub_rn(__dadd_rn(g, x), a.U_sub[b * a.ld_sub + i]) : __dadd_rn(x, g);
+                w[i] = x;
+                if (a.out) a.out[b * a.ld_out + i] = x;
+            });
+            reduce_nodes([&](int64_t i) { return __dmul_rn(w[i], w[i]); });
+        }
+        const double tot = gtotal();
+        if (active && tid == 0 && chunk == 0) {
+            if (a.partial) a.partial[b] = tot;    // per-row sum of squares
+            if (C.gmres_iters) C.gmres_iters[b] = anybad ? -1 : done;
+        }
+        grid.sync();
+    }
+}
+
+int tiles_for(int64_t n) { return (int)((n + kTile2 - 1) / kTile2); }
+
+int coop_capacity(const void *fn) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kNT2, 0) != cudaSuccess || per < 1) per = 1;
+    return sms * per;
+}
+
+template <typename Fn>
+int dispatch_p(int p, Fn &&f) {
+    switch (p) {
+        case 1: return f(std::integral_constant<int, 1>{});
+        case 3: return f(std::integral_constant<int, 3>{});
+        default: return f(std::integral_constant<int, 5>{});
+    }
+}
+
+}  // namespace
+
+int64_t capacity2d(const mgrit_level_desc *L) {
+    if (L->kind != MGRIT_KIND_CORRECTED) return (int64_t)1 << 30;
+    return dispatch_p(L->p, [&](auto PP) {
+        constexpr int P = decltype(PP)::value;
+        return coop_capacity((const void *)gmres2d_coop<P>);
+    });
+}
+
+static int64_t coop_row_bytes(const mgrit_level_desc *L) {
+    const int64_t n = L->n_points, nwb = (n + kWB - 1) / kWB;
+    return 8 * ((int64_t)(L->gmres_max_iters + 2) * n + 2 * nwb) + 4 * 4096 + 4;
+}
+
+int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows) {
+    const int64_t n = L->n_points;
+    if (L->kind == MGRIT_KIND_CORRECTED) {
+        const int64_t r = rows < 1 ? 1 : rows;
+        return r * coop_row_bytes(L) + 4096;
+    }
+    // FE needs the SL rows; all kinds need tile partials for row norms
+    const int64_t r = rows < 1 ? 1 : rows;
+    return (L->kind == MGRIT_KIND_FORWARD_EULER ? 8 * r * n : 0) + 8 * r * tiles_for(n) + 256;
+}
+
+static int validate2d(const mgrit_level_desc *L) {
+    if (!L || L->dim != 2 || L->n_x < 8 || !L->s_x || !L->s_y) return MGRIT_EINVAL;
+    if (L->p != 1 && L->p != 3 && L->p != 5) return MGRIT_EINVAL;
+    if (L->kind < 0 || L->kind > 2) return MGRIT_EINVAL;
+    if (L->kind != MGRIT_KIND_SL && (!L->sig_x || !L->sig_y)) return MGRIT_EINVAL;
+    if (L->kind == MGRIT_KIND_CORRECTED && (L->gmres_max_iters < 1 || L->gmres_max_iters > kMaxK2))
+        return MGRIT_EINVAL;
+    return MGRIT_OK;
+}
+
+int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, int64_t scratch_bytes,
+                  int32_t *status, cudaStream_t st) {
+    int rc = validate2d(L);
+    if (rc) return rc;
+    if (r.B <= 0) return MGRIT_OK;
+    const int64_t n = L->n_points;
+    const int tiles = tiles_for(n);
+    Rows2D a{r.B, r.t_idx, r.t_first, r.t_stride, r.U_in, r.ld_in, r.G, r.ld_g, r.U_sub, r.ld_sub,
+             r.out, r.ld_out, nullptr};
+    char *scr = (char *)scratch;
+    if (L->kind == MGRIT_KIND_CORRECTED) {
+        return dispatch_p(L->p, [&](auto PP) {
+            constexpr int P = decltype(PP)::value;
+            const void *fn = (const void *)gmres2d_coop<P>;
+            const int G = coop_capacity(fn);
+            int64_t rows = r.B < G ? r.B : G;
+            const int64_t per_row = coop_row_bytes(L);
+            if (scratch_bytes - 4096 < per_row) return (int)MGRIT_EINVAL;
+            if (rows > (scratch_bytes - 4096) / per_row) rows = (scratch_bytes - 4096) / per_row;
+            int chunks = (int)(G / rows);
+            if (chunks < 1) chunks = 1;
+            while ((int64_t)chunks * rows > 4096) --chunks;
+            const int64_t nwb = (n + kWB - 1) / kWB;
+            Coop2D C;
+            C.L = *L;
+            C.a = a;
+            C.a.partial = r.row_sumsq;
+            C.rows_per_round = rows;
+            C.chunks = chunks;
+            C.nwb = nwb;
+            C.basis = (double *)scr;
+            C.w = C.basis + rows * (int64_t)(L->gmres_max_iters + 1) * n;
+            C.part = C.w + rows * n;
+            C.flags = (int *)(C.part + 2 * rows * nwb);
+            C.stopflags = C.flags + rows * chunks;
+            C.gmres_iters = r.gmres_iters;
+            C.status = status;
+            void *args[] = {&C};
+            const int grid = (int)(rows * chunks);
+            cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kNT2, args, 0, st);
+            if (e != cudaSuccess) {
+                set_error("gmres2d_coop", e);
+                return (int)MGRIT_ECUDA;
+            }
+            return check_launch("gmres2d_coop");
+        });
+    }
+    double *partial = nullptr;
+    double *V = nullptr;
+    if (L->kind == MGRIT_KIND_FORWARD_EULER) {
+        V = (double *)scr;
+        scr += 8 * r.B * n;
+    }
+    if (r.row_sumsq) partial = (double *)scr;
+    const int64_t need = (V ? 8 * r.B * n : 0) + (partial ? 8 * r.B * tiles : 0);
+    if (need > scratch_bytes) return MGRIT_EINVAL;
+    const dim3 grid((unsigned)tiles, (unsigned)r.B);
+    return dispatch_p(L->p, [&](auto PP) {
+        constexpr int P = decltype(PP)::value;
+        if (L->kind == MGRIT_KIND_FORWARD_EULER) {
+            Rows2D s = a;
+            s.out = V;
+            s.ld_out = n;
+            sl2d_kernel<P, true><<<grid, kNT2, 0, st>>>(*L, s);
+            Rows2D f = a;
+            f.partial = partial;
+            fe2d_kernel<P><<<grid, kNT2, 0, st>>>(*L, f, V);
+        } else {
+            Rows2D s = a;
+            s.partial = partial;
+            sl2d_kernel<P, false><<<grid, kNT2, 0, st>>>(*L, s);
+        }
+        if (partial) rowsum_kernel<<<(unsigned)(r.B < 4096 ? r.B : 4096), kNT2, 0, st>>>(partial, tiles, r.B, r.row_sumsq);
+        return check_launch("apply_rows_2d");
+    });
+}
+
+// ---------------------------------------------------------------------------
+// fused phases for 2D, composed from batched row launches
+
+static int copy_rows(double *dst, int64_t ld_dst, const double *src, int64_t ld_src, int64_t rows, int64_t n,
+                     cudaStream_t st) {
+    if (rows <= 0) return MGRIT_OK;
+    cudaError_t e = cudaMemcpy2DAsync(dst, ld_dst * 8, src, ld_src * 8, n * 8, rows, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+        set_error("cudaMemcpy2DAsync", e);
+        return MGRIT_ECUDA;
+    }
+    return MGRIT_OK;
+}
+
+static int zero_rows(double *dst, int64_t ld, int64_t rows, int64_t n, cudaStream_t st) {
+    if (rows <= 0) return MGRIT_OK;
+    cudaError_t e = cudaMemset2DAsync(dst, ld * 8, 0, n * 8, rows, st);
+    if (e != cudaSuccess) {
+        set_error("cudaMemset2DAsync", e);
+        return MGRIT_ECUDA;
+    }
+    return MGRIT_OK;
+}
+
+int axpy_rows_impl(double *U, int64_t ldu, int64_t stride, const double *X, int64_t ldx, int64_t rows,
+                   int64_t n, cudaStream_t st);
+
+int level_phase_2d(const mgrit_level_desc *L, const mgrit_phase_args *A, void *scratch, int64_t scratch_bytes,
+                   int32_t *status, cudaStream_t st) {
+    int rc = validate2d(L);
+    if (rc) return rc;
+    if (!A || A->m < 1 || !A->U || !A->Cbuf || A->c_count < 0 || A->n_intervals < 1) return MGRIT_EINVAL;
+    if ((int64_t)A->n_intervals * A->m != L->n_steps) return MGRIT_EINVAL;
+    if (A->c_count == 0) return MGRIT_OK;
+    const int64_t n = L->n_points, m = A->m, cb = A->c_begin, cnt = A->c_count;
+    const int64_t ldm = m * A->ldu;
+    auto Urow = [&](int64_t t) { return A->U + (t - A->u_row0) * A->ldu; };
+    auto Grow = [&](int64_t t) -> const double * { return A->G ? A->G + (t - A->g_row0) * A->ldg : nullptr; };
+    auto Crow = [&](int64_t c) { return A->Cbuf + (c - A->c_row0) * n; };
+    auto Ucrow = [&](int64_t c) { return A->Uc + (c - A->c_row0) * n; };
+    const int64_t ldgm = m * A->ldg;
+    auto steps = [&](int64_t k, double *out, int64_t ld_out, const double *Usub, int64_t ld_sub, double *rss) {
+        // rows t = c*m + k - 1 -> out; forcing G[c*m + k]
+        RowsArgs r{cnt, nullptr, cb * m + k - 1, m, Urow(cb * m + k - 1), ldm, Grow(cb * m + k), ldgm,
+                   Usub, ld_sub, out, ld_out, rss, nullptr};
+        return apply_rows_2d(L, r, scratch, scratch_bytes, status, st);
+    };
+    const int phase = A->phase;
+    // ---- left states
+    if (phase == MGRIT_PHASE_FC || phase == MGRIT_PHASE_FONLY_RES) {
+        if (A->zero_init && (rc = zero_rows(Urow(cb * m), ldm, cnt, n, st))) return rc;
+    } else if (phase == MGRIT_PHASE_F_RES) {
+        if (A->zero_init && cb == 0 && (rc = zero_rows(Urow(0), A->ldu, 1, n, st))) return rc;
+        const int64_t c_lo = cb > 0 ? cb : 1;
+        if ((rc = copy_rows(Urow(c_lo * m), ldm, Crow(c_lo), n, cb + cnt - c_lo, n, st))) return rc;
+    } else if (phase == MGRIT_PHASE_INJ_F) {
+        // U[c m] += Uc[c] for c in [cb, cb+cnt] (the right edge too, on this
+        // rank's copy, so the C-point residual of its last interval is current)
+        if ((rc = axpy_rows_impl(Urow(cb * m), A->ldu, m, Ucrow(cb), n, cnt + 1, n, st))) return rc;
+    }
+    // ---- F-relaxation
+    for (int64_t k = 1; k < m; ++k)
+        if ((rc = steps(k, Urow(cb * m + k), ldm, nullptr, 0, nullptr))) return rc;
+    // ---- tails
+    if (phase == MGRIT_PHASE_FC) {
+        RowsArgs r{cnt, nullptr, cb * m + m - 1, m, Urow(cb * m + m - 1), ldm, Grow(cb * m + m), ldgm,
+                   nullptr, 0, Crow(cb + 1), n, nullptr, nullptr};
+        return apply_rows_2d(L, r, scratch, scratch_bytes, status, st);
+    }
+    if (phase == MGRIT_PHASE_F_RES) {
+        if ((rc = copy_rows(Urow((cb + 1) * m), ldm, Crow(cb + 1), n, cnt, n, st))) return rc;
+    } else if (phase == MGRIT_PHASE_FONLY_RES) {
+        if (A->zero_init && (rc = zero_rows(Urow((cb + 1) * m), ldm, cnt, n, st))) return rc;
+        if ((rc = copy_rows(Crow(cb + 1), n, Urow((cb + 1) * m), ldm, cnt, n, st))) return rc;
+    } else if (phase == MGRIT_PHASE_INJ_F && !A->partial) {
+        return MGRIT_OK;
+    }
+    double *out = (phase == MGRIT_PHASE_INJ_F || !A->Gc) ? nullptr : A->Gc + (cb + 1 - A->c_row0) * n;
+    double *rss = A->partial ? A->partial + (cb - A->partial0) : nullptr;
+    if (!out && !rss) return MGRIT_OK;
+    return steps(m, out, n, Urow((cb + 1) * m), ldm, rss);
+}
+
+int sweep_2d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg, int zero_init,
+             int32_t *gmres_iters, void *scratch, int64_t scratch_bytes, int32_t *status, cudaStream_t st) {
+    int rc = validate2d(L);
+    if (rc) return rc;
+    const int64_t n = L->n_points;
+    if (zero_init && (rc = zero_rows(U, ldu, 1, n, st))) return rc;
+    for (int64_t t = 0; t < L->n_steps; ++t) {
+        RowsArgs r{1, nullptr, t, 1, U + t * ldu, ldu, G ? G + (t + 1) * ldg : nullptr, ldg, nullptr, 0,
+                   U + (t + 1) * ldu, ldu, nullptr, gmres_iters ? gmres_iters + t : nullptr};
+        if ((rc = apply_rows_2d(L, r, scratch, scratch_bytes, status, st))) return rc;
+    }
+    return MGRIT_OK;
+}
+
+}  // namespace mgrit

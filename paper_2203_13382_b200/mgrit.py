@@ -621,7 +621,7 @@ class _FusedCycle:
 
 
 def _fused_ok(levels):
-    return all(lv.kind != "ideal" and lv.grid.dim == 1 for lv in levels)
+    return all(lv.kind != "ideal" for lv in levels)
 
 
 def initial_state(cfg: SolverConfig, grid) -> np.ndarray:
@@ -653,7 +653,7 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
     n = grid.n_points
     use_fused = (engine == "fused") or (engine == "auto" and _fused_ok(levels))
     if use_fused and not _fused_ok(levels):
-        raise ValueError("fused engine supports 1D non-ideal hierarchies")
+        raise ValueError("fused engine needs a hierarchy without ideal levels")
     sess = _session(levels, cfg, dev) if use_fused else None
     U = sess.U if sess is not None else torch.empty((cfg.n_t + 1, n), dtype=torch.float64, device=dev)
     U[0] = torch.from_numpy(initial_state(cfg, grid)).to(dev)

@@ -245,6 +245,9 @@ def _check_solve(rep, U, info, g, exact_records, name=None):
         assert _rel(U[:: info["row_stride"]], g["U_rows"]) <= utol
 
 
+SOLVES_2D = ["tiny2d_C5_p3_m4", "tiny2d_B4_p3_m4", "cfg4_reduced", "cfg5_reduced", "crit3_C4_p1_m4",
+             "crit3_C4_p3_m4", "crit3_C4_p5_m16", "crit3_C5_p1_m4"]
+
 SOLVES_1D = ["tiny1d_C3_p3_m4", "tiny1d_B2_p5_m8", "tiny1d_C1_2lvl_pm1", "kind_F_relax", "kind_ideal",
              "kind_rediscretized", "kind_forward_euler", "kind_erk_substeps", "kind_schedule_16_4",
              "kind_diverge", "crit1_C1_p1_m4", "crit1_C1_p1_m8", "crit1_C1_p1_m16", "crit1_C1_p3_m4",
@@ -255,6 +258,15 @@ SOLVES_1D = ["tiny1d_C3_p3_m4", "tiny1d_B2_p5_m8", "tiny1d_C1_2lvl_pm1", "kind_F
 @pytest.mark.parametrize("name", SOLVES_1D)
 def test_solve_matches_reference_golden(P, golden_index, name):
     """Device ERK + device hierarchy + fused engine vs the reference's history."""
+    info = golden_index[name]
+    g = load_solve(name)
+    rep, U = P.solve(P.SolverConfig(**info["kw"]))
+    _check_solve(rep, U, info, g, exact_records=False, name=name)
+
+
+@pytest.mark.parametrize("name", SOLVES_2D)
+def test_solve_2d_matches_reference_golden(P, golden_index, name):
+    """2D: device ERK + device hierarchy + fused 2D phases vs the reference's history."""
     info = golden_index[name]
     g = load_solve(name)
     rep, U = P.solve(P.SolverConfig(**info["kw"]))
@@ -356,3 +368,90 @@ def test_time_parallel_engine_single_rank_equals_fused(P):
         assert np.array_equal(U1, _np(U2))
         assert np.array_equal(r1.residual_norms, r2.residual_norms)
         assert r1.status == r2.status
+
+
+@pytest.mark.parametrize("p", [1, 3, 5])
+@pytest.mark.parametrize("speed", ["C4", "C5", "B4"])
+def test_sl_step_batch_2d_bitwise(P, p, speed):
+    """2D tensor-product SL step and the strided relax/residual operators are
+    bit-identical to the reference (x inner, y outer, from zero)."""
+    kw = dict(n_x=24, n_t=16, dim=2, wave_speed=speed, p=p, schedule=4)
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, olevels = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    rng = np.random.default_rng(17)
+    U = rng.standard_normal((16, 24 * 24))
+    t = np.arange(16)
+    got = _np(levels[0].step_batch(t, torch.from_numpy(U).to(dev())))
+    assert np.array_equal(got, olevels[0].step_batch(t, U))
+    G = rng.standard_normal((17, 576))
+    U0 = rng.standard_normal((17, 576))
+    for fn_d, fn_o in ((P.f_relax, O.f_relax), (P.c_relax, O.c_relax)):
+        Ud = torch.from_numpy(U0.copy()).to(dev())
+        Uo = U0.copy()
+        fn_d(levels[0], Ud, torch.from_numpy(G).to(dev()))
+        fn_o(olevels[0], Uo, G)
+        assert np.array_equal(_np(Ud), Uo)
+    Rd = P.residual(levels[0], torch.from_numpy(U0).to(dev()), torch.from_numpy(G).to(dev()))
+    assert np.array_equal(_np(Rd), O.residual(olevels[0], U0, G))
+
+
+@pytest.mark.parametrize("p", [1, 3, 5])
+@pytest.mark.parametrize("mode", ["fixed", "tolerance"])
+def test_corrected_step_2d_matches_oracle(P, p, mode):
+    """2D corrected operator (cooperative grid-wide MGS-GMRES): rows within
+    1e-13 of the reference's and identical per-call GMRES counts."""
+    kw = dict(n_x=16, n_t=64, dim=2, wave_speed="C5", p=p, schedule=4, gmres_mode=mode)
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, olevels = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    rng = np.random.default_rng(23)
+    for li in (1, 2):
+        lv, ol = levels[li], olevels[li]
+        U = rng.standard_normal((lv.n_steps, 256))
+        log = O.GmresLog()
+        ol.log = log
+        want = ol.step_batch(np.arange(lv.n_steps), U)
+        iters = torch.zeros(lv.n_steps, dtype=torch.int32, device=dev())
+        out = torch.empty((lv.n_steps, 256), dtype=torch.float64, device=dev())
+        lv._apply(torch.from_numpy(U).to(dev()), 0, 0, lv.n_steps, out,
+                  t_idx=torch.arange(lv.n_steps, device=dev()), gmres_iters=iters)
+        assert _rel(_np(out), want) < 1e-13
+        assert list(_np(iters)) == log.counts
+
+
+def test_forward_euler_2d_bitwise(P):
+    kw = dict(n_x=16, n_t=64, dim=2, wave_speed="C5", p=3, schedule=4, operator_kind="forward_euler",
+              max_levels=2)
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, olevels = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    U = np.random.default_rng(3).standard_normal((16, 256))
+    t = np.arange(16)
+    assert np.array_equal(_np(levels[1].step_batch(t, torch.from_numpy(U).to(dev()))),
+                          olevels[1].step_batch(t, U))
+
+
+@pytest.mark.parametrize("name", ["tiny2d_C5_p3_m4", "tiny2d_B4_p3_m4"])
+def test_per_iteration_snapshots_2d(P, golden_index, name):
+    info = golden_index[name]
+    g = load_solve(name)
+    kw = info["kw"]
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, _ = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    snaps = g["snaps"]
+    for k in range(1, len(snaps) + 1):
+        rep, U = P.solve(P.SolverConfig(**{**kw, "max_iters": k, "rtol": 0.0}), levels)
+        assert _rel(U, snaps[k - 1]) <= U_TOL, k
+
+
+def test_fused_2d_equals_reference_structured_path(P):
+    for kw in (dict(n_x=16, n_t=64, dim=2, wave_speed="B4", p=3, schedule=4, u0="sin4", seed=3),
+               dict(n_x=16, n_t=64, dim=2, wave_speed="C5", p=1, schedule=4, relaxation="F")):
+        cfg = P.SolverConfig(**{**kw, "max_iters": 3, "rtol": 0.0})
+        levels = P.build_hierarchy(cfg)
+        r1, U1 = P.solve(cfg, levels, engine="fused")
+        r2, U2 = P.solve(cfg, levels, engine="reference")
+        assert np.array_equal(U1, U2), kw
+        assert np.allclose(r1.residual_norms, r2.residual_norms, rtol=1e-13, atol=0)
