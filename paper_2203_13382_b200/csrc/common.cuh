@@ -40,11 +40,19 @@ struct Dec {
 
 // east = ceil(s), eps = east - s, rounding guards, east mod n.
 // s = mod(x - x_lo, L)/h lies in [0, n], so east in [-1, n] before the
-// periodic wrap: two compares instead of an integer division.
+// periodic wrap: two compares instead of an integer division.  ceil and the
+// int conversion avoid the low-throughput XU pipe (FRND / F2I): for
+// 0 <= s < 2^52, t = s + 2^52 rounds s to the nearest integer r, exactly
+// stored in t's low mantissa bits; ceil(s) = r or r + 1.  Same bits as ceil().
 __device__ __forceinline__ Dec decompose_s(double s, int n) {
-    const double ef = ceil(s);
+    const double t = __dadd_rn(s, 4503599627370496.0);  // 2^52
+    int e = __double2loint(t);
+    double ef = __dsub_rn(t, 4503599627370496.0);        // exact: nearest integer to s
+    if (ef < s) {
+        ef = __dadd_rn(ef, 1.0);
+        e += 1;
+    }
     double eps = __dsub_rn(ef, s);
-    int e = (int)ef;
     if (eps < 0.0) eps = 0.0;
     if (eps >= 1.0) {
         eps = __dsub_rn(eps, 1.0);
@@ -167,6 +175,16 @@ __device__ __forceinline__ double cmul(int idx, double x) {
     if (c == -1.0) return -x;
     return __dmul_rn(c, x);
 }
+
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS) staging of one fp64 per thread into shared memory
+
+__device__ __forceinline__ void cp_async8(double *smem_dst, const double *gmem_src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // deterministic reductions

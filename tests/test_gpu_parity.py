@@ -455,3 +455,18 @@ def test_fused_2d_equals_reference_structured_path(P):
         r2, U2 = P.solve(cfg, levels, engine="reference")
         assert np.array_equal(U1, U2), kw
         assert np.allclose(r1.residual_norms, r2.residual_norms, rtol=1e-13, atol=0)
+
+
+def test_large_row_n16384_matches_oracle(P):
+    """n_x = 16384 (config 3's mesh) uses the widest row configuration
+    (1024 threads x 16 nodes per row, corrected levels included): full solve
+    against the oracle at a short time horizon."""
+    kw = dict(n_x=16384, n_t=256, wave_speed="B2", p=5, schedule=8, seed=2, max_iters=6, rtol=0.0)
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, olevels = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    rep, U = P.solve(cfg, levels)
+    orep, oU = O.solve(ocfg, olevels)
+    r0 = orep.residual_norms[0]
+    assert np.all(np.abs(rep.residual_norms - orep.residual_norms) <= 1e-12 * r0)
+    assert _rel(U, oU) <= U_TOL
