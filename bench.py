@@ -262,6 +262,18 @@ def run_gpu(args):
                 "ms_per_launch": round(tb["ms_avg"], 5), "peak_source": peak["source"],
                 "share_of_iteration": round(tb["ms_total"] / sum(v["ms_total"] for v in breakdown.values()), 3)}
 
+    # the SL-step kernel itself (BASELINE: "SL-step HBM GB/s"): the fine-level
+    # F+C relaxation phase (plain semi-Lagrangian steps, G = 0)
+    sl_key = next((k for k in breakdown if k.startswith("L0_FC") or k.startswith("L0_FONLY")), None)
+    sl_roof = None
+    if sl_key is not None:
+        sb = breakdown[sl_key]
+        ach = sb["bytes"] / (sb["ms_avg"] / 1e3) / 1e9
+        sl_roof = {"bound": "hbm", "kernel": sl_key, "achieved": round(ach, 1), "peak": peak["hbm_gbs"],
+                   "unit": "GB/s", "frac": round(ach / peak["hbm_gbs"], 4), "traffic": _ncu_traffic(sl_key),
+                   "bytes_per_launch": sb["bytes"], "ms_per_launch": round(sb["ms_avg"], 5),
+                   "note": "plain SL steps of the fine level; also FP64-issue bound (~32 FP64 ops per node-update)"}
+
     # ---- sequential GPU time stepping (fine level, one CTA walks all steps)
     for _ in range(2):
         P.sequential_reference(cfg, levels, output="device")
@@ -299,6 +311,7 @@ def run_gpu(args):
                              f"{8 * cfg.dim * cfg.n_t * npts / 1e6:.0f} MB > 126 MB)",
                        "setup_s": round(setup_s, 4), "iterations": iters, "status": rep.status},
             "roofline": roofline,
+            "sl_step_roofline": sl_roof,
             "cpu_baseline": cpu,
             "e2e": {"value": n_dof / (e2e / 1e3), "unit": "DOF/s", "ms_per_step": e2e,
                     "h2d_bytes_per_step": int(Xp.numel() * 8 + npts * 8) * world,
@@ -316,8 +329,12 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def kernel_breakdown(levels, cfg, reps: int = 3):
-    """Time every launch of one V-cycle with CUDA events on the launching stream."""
+def kernel_breakdown(levels, cfg, inner: int = 5, reps: int = 3):
+    """Device time of every launch of one V-cycle: each launch (in cycle order)
+    is captured `inner` times into its own CUDA graph and replayed between CUDA
+    events on the launching stream, so host launch overhead is excluded.
+    Repeating a phase is harmless for timing (the phases are idempotent except
+    INJ_F, whose repeated injection only changes values)."""
     import torch
     from paper_2203_13382_b200 import _lib
     from paper_2203_13382_b200 import mgrit as M
@@ -326,54 +343,48 @@ def kernel_breakdown(levels, cfg, reps: int = 3):
     U[0] = 0.5
     M.pcg64_uniform(cfg.seed, cfg.n_t, levels[0].grid.n_points, U[1:])
     eng = M._FusedCycle(levels, U, cfg.relaxation)
+    eng.iteration()                     # realistic state + kernel attributes set
+    torch.cuda.synchronize()
     names = {_lib.PHASE_FC: "FC", _lib.PHASE_F_RES: "F_RES", _lib.PHASE_FONLY_RES: "FONLY_RES",
              _lib.PHASE_INJ_F: "INJ_F"}
-    rec = {}
-    orig_phase = eng._phase
-    stream = torch.cuda.current_stream()
-    count = [0]
+    order = []
 
-    def timed_phase(li, ph):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        orig_phase(li, ph)
-        b.record(stream)
-        key = f"L{li}_{names[ph]}_{levels[li].kind}"
-        rec.setdefault(key, []).append((a, b, phase_bytes(levels[li], ph, li == 0)))
-        count[0] += 1
-
-    eng._phase = timed_phase
-    orig_cycle = eng.cycle
-
-    def timed_cycle(li=0):
+    def walk(li=0):
         if li == len(levels) - 1:
+            order.append((f"L{li}_sweep_{levels[li].kind}", lambda li=li: eng.cycle(li), 0))
+            return
+        seq = [_lib.PHASE_FC, _lib.PHASE_F_RES] if eng.relaxation == "FCF" else [_lib.PHASE_FONLY_RES]
+        for ph in seq:
+            order.append((f"L{li}_{names[ph]}_{levels[li].kind}", lambda li=li, ph=ph: eng._phase(li, ph),
+                          phase_bytes(levels[li], ph, li == 0)))
+        walk(li + 1)
+        ph = _lib.PHASE_INJ_F
+        order.append((f"L{li}_{names[ph]}_{levels[li].kind}", lambda li=li, ph=ph: eng._phase(li, ph),
+                      phase_bytes(levels[li], ph, li == 0)))
+
+    walk()
+    out = {}
+    stream = torch.cuda.current_stream()
+    for key, fn, nbytes in order:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(inner):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            orig_cycle(li)
+            g.replay()
             b.record(stream)
-            rec.setdefault(f"L{li}_sweep_{levels[li].kind}", []).append((a, b, 0))
-            count[0] += 1
-            return
-        _cycle_body(li)
-
-    def _cycle_body(li):
-        if eng.relaxation == "FCF":
-            eng._phase(li, _lib.PHASE_FC)
-            eng._phase(li, _lib.PHASE_F_RES)
-        else:
-            eng._phase(li, _lib.PHASE_FONLY_RES)
-        timed_cycle(li + 1)
-        eng._phase(li, _lib.PHASE_INJ_F)
-
-    for _ in range(reps):
-        count[0] = 0
-        timed_cycle(0)
-        torch.cuda.synchronize()
-    out = {}
-    for k, lst in rec.items():
-        ms = [a.elapsed_time(b) for a, b, _ in lst]
-        out[k] = {"ms_total": float(np.sum(ms)) / reps, "ms_avg": float(np.mean(ms)), "bytes": lst[0][2]}
-    return out, count[0] + 1   # + the norm sum
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / inner)
+        ms = float(np.median(ts))
+        o = out.setdefault(key, {"ms_total": 0.0, "ms_avg": ms, "bytes": nbytes, "launches": 0})
+        o["ms_total"] += ms
+        o["launches"] += 1
+    return out, len(order) + 1   # + the norm sum
 
 
 def _peak():

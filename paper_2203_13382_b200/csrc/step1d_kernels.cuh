@@ -267,27 +267,29 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                     }
                 }
                 double hrun = 0.0;  // thread 0: column kk entry j after rotations < j
-#pragma unroll 1
-                for (int j = 0; j <= kk; ++j) {
-                    double a4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                    for (int k = 0; k < NPT; ++k) a4[k & 3] = fma(bc[k], v[k], a4[k & 3]);
-                    const double part = __dadd_rn(__dadd_rn(a4[0], a4[1]), __dadd_rn(a4[2], a4[3]));
-                    double bn[NPT];
+                // one MGS step on (cur = b_j in registers); nxt receives b_{j+1}
+                // (loads issued first so they overlap the FMAs and the reduction)
+                auto mgs_step = [&](int j, double (&cur)[NPT], double (&nxt)[NPT]) {
                     if (j < kk) {
                         const double *bp = j + 1 == kk ? cx.rowbuf : cx.bvec(j + 1, n);
 #pragma unroll
                         for (int k = 0; k < NPT; ++k) {
                             const int i = tid + k * NT;
-                            bn[k] = (F || i < n) ? bp[i] : 0.0;
+                            nxt[k] = (F || i < n) ? bp[i] : 0.0;
                         }
                     }
+                    double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int k = 0; k < NPT; ++k) a4[k & 3] = fma(cur[k], v[k], a4[k & 3]);
+                    const double part = __dadd_rn(__dadd_rn(a4[0], a4[1]), __dadd_rn(a4[2], a4[3]));
                     double c = 0.0, sn = 0.0;
                     if (tid == 0 && j > 0) {
                         c = G.cs[j - 1];
                         sn = G.sn[j - 1];
                     }
+                    if (kk == 5) MGRIT_PROBE_AT(301 + 4 * j);
                     const double h = block_sum2<NT>(part, cx);
+                    if (kk == 5) MGRIT_PROBE_AT(302 + 4 * j);
                     if (tid == 0) {
                         if (j == 0) {
                             hrun = h;
@@ -299,10 +301,14 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                         }
                     }
 #pragma unroll
-                    for (int k = 0; k < NPT; ++k) {
-                        v[k] = fma(-h, bc[k], v[k]);
-                        bc[k] = bn[k];
-                    }
+                    for (int k = 0; k < NPT; ++k) v[k] = fma(-h, cur[k], v[k]);
+                    if (kk == 5) MGRIT_PROBE_AT(303 + 4 * j);
+                };
+                double bo[NPT];
+#pragma unroll 1
+                for (int j = 0; j <= kk; j += 2) {
+                    mgs_step(j, bc, bo);
+                    if (j + 1 <= kk) mgs_step(j + 1, bo, bc);
                 }
                 MGRIT_PROBE_AT(12 + 8 * kk);
                 const double nrm = sqrt(block_sum2<NT>(sumsq4(), cx));
@@ -431,9 +437,11 @@ __device__ __forceinline__ double residual_form(double (&v)[NPT], const double *
     return ss;
 }
 
-// dynamic shared memory: [halo | rowbuf n | halo][GmresSmem][nbs Krylov slots of n]
+// dynamic shared memory: [halo | rowbuf n | halo][GmresSmem][nbs slots of n][2*kHalo]
 __host__ __device__ inline size_t smem_bytes_for(int n, int nbs) {
-    return sizeof(double) * ((size_t)n + 2 * kHalo) + sizeof(GmresSmem) + sizeof(double) * (size_t)n * nbs;
+    // the trailing 2*kHalo doubles give the SL path's second row buffer its halo
+    return sizeof(double) * ((size_t)n + 2 * kHalo) + sizeof(GmresSmem) +
+           sizeof(double) * ((size_t)n * nbs + 2 * kHalo);
 }
 
 __device__ __forceinline__ RowCtx make_ctx(double *sm, int n, int nbs, double *scratch, int64_t slot,
@@ -502,6 +510,11 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
     const int m = A.m;
     RowCtx cx = make_ctx(sm, n, nbs, scratch, blockIdx.x, L, status);
     double *recbuf = cx.bsm;  // n doubles (ASYNC only)
+    // ASYNC (plain SL): the row is double-buffered, so each step needs one
+    // barrier (write the other buffer, sync, swap) instead of two.
+    // layout after GmresSmem: [recbuf n][halo | rowB n | halo]
+    double *const rowA = cx.rowbuf;
+    double *const rowB = cx.bsm + n + kHalo;
     auto stage = [&](int64_t t) {
         const double *s = L.s_x + (L.shared ? 0 : t) * (int64_t)n;
 #pragma unroll
@@ -552,6 +565,7 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
         } else if (A.phase == MGRIT_PHASE_F_RES && c > 0) {
             store_row<NT, NPT, F>(U(t0), v, n);
         }
+        if constexpr (ASYNC) cx.rowbuf = rowA;
         set_row<NT, NPT, F>(cx.rowbuf, v, n);
 
         // ---- F-relaxation chain (mgrit.py:276-283) then the interval tail at
@@ -588,7 +602,18 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
             if (k < m) {
                 add_forcing<NT, NPT, F>(v, Gr(t), n);
                 store_row<NT, NPT, F>(U(t), v, n);
-                set_row<NT, NPT, F>(cx.rowbuf, v, n);
+                if constexpr (ASYNC) {
+                    double *other = cx.rowbuf == rowB ? rowA : rowB;
+#pragma unroll
+                    for (int q = 0; q < NPT; ++q) {
+                        const int i = threadIdx.x + q * NT;
+                        if (F || i < n) put_row(other, i, v[q], n);
+                    }
+                    __syncthreads();
+                    cx.rowbuf = other;
+                } else {
+                    set_row<NT, NPT, F>(cx.rowbuf, v, n);
+                }
                 continue;
             }
             // ---- interval tail at the right C-point tC = t
@@ -710,7 +735,9 @@ inline int max_smem_optin() {
 
 // Krylov slots that fit in shared memory next to the row
 inline int smem_slots(const mgrit_level_desc *L) {
-    if (L->kind == MGRIT_KIND_SL) return L->n_x <= 8192 ? 1 : 0;  // cp.async record staging buffer
+    // plain SL: cp.async record staging buffer + second row buffer (its halo
+    // comes from the 2*kHalo spare doubles smem_bytes_for always reserves)
+    if (L->kind == MGRIT_KIND_SL) return L->n_x <= 8192 ? 2 : 0;
     if (L->kind != MGRIT_KIND_CORRECTED) return 0;
     const int64_t base = (int64_t)smem_bytes_for(L->n_x, 0);
     const int64_t avail = (int64_t)max_smem_optin() - base - 1024;

@@ -126,3 +126,25 @@ def test_product_fails_loudly_without_cuda():
         pytest.skip("CUDA present")
     with pytest.raises(RuntimeError, match="CUDA"):
         build_hierarchy(SolverConfig(n_x=16, n_t=16))
+
+
+def test_cli_parse_and_config(tmp_path):
+    from paper_2203_13382_b200 import cli
+    assert cli.parse_size("(2^6)^2x2^10") == 2 ** 22
+    with pytest.raises(ValueError):
+        cli.parse_size("2^x")
+    cfgf = tmp_path / "c.json"
+    cfgf.write_text('{"n_x": 64, "n_t": 128, "p": 3, "wave_speed": "C3"}')
+    parser = cli.build_parser()
+    argv = ["run", "--config", str(cfgf), "-p", "5"]
+    args = parser.parse_args(argv)
+    args.explicit = cli._explicit_dests(parser._run_parser, argv)
+    cfg = cli.config_from_namespace(args)
+    assert (cfg.n_x, cfg.n_t, cfg.p, cfg.wave_speed) == (64, 128, 5, "C3")
+    bad = tmp_path / "b.json"
+    bad.write_text('{"n_x": 64, "n_t": 128, "bogus": 1}')
+    args = parser.parse_args(["run", "--config", str(bad)])
+    args.explicit = set()
+    with pytest.raises(ValueError):
+        cli.config_from_namespace(args)
+    assert cli.main(["run", "--config", str(bad)]) == 2

@@ -470,3 +470,17 @@ def test_large_row_n16384_matches_oracle(P):
     r0 = orep.residual_norms[0]
     assert np.all(np.abs(rep.residual_norms - orep.residual_norms) <= 1e-12 * r0)
     assert _rel(U, oU) <= U_TOL
+
+
+def test_cli_run_report_matches_reference_format(P, tmp_path, golden_index):
+    """`run` writes the reference's JSON/CSV report (cli.py:139-157)."""
+    import json
+    from paper_2203_13382_b200 import cli
+    out = str(tmp_path / "r")
+    assert cli.main(["run", "--nx", "32", "--nt", "64", "--wave-speed", "C3", "-p", "3", "-o", out]) == 0
+    rep = json.load(open(out + ".json"))
+    assert set(rep) == {"config", "iterations", "status", "final_factor", "wall_time", "residual_norms"}
+    g = load_solve("tiny1d_C3_p3_m4")
+    assert rep["iterations"] == golden_index["tiny1d_C3_p3_m4"]["iterations"]
+    assert np.allclose(rep["residual_norms"], g["hist"], rtol=0, atol=1e-12 * g["hist"][0])
+    assert open(out + ".csv").readline().strip() == "iteration,residual_norm"

@@ -52,5 +52,11 @@ int main(int argc, char **argv) {
                q[6] - q[5], q[6] - q[0]);
     }
     printf(" xcomb %lld   total %lld cycles\n", h[201] - h[200], h[201] - h[0]);
+    if (K > 5)
+        for (int j = 0; j <= 5; ++j) {
+            long long *q = h + 300 + 4 * j;
+            printf("  kk=5 j=%d: dot->prefetch-issued %lld, prefetch->h %lld (reduction), h->axpy-done %lld, next-dot %lld\n",
+                   j, q[1] - q[0], q[2] - q[1], q[3] - q[2], j < 5 ? q[4] - q[3] : 0LL);
+        }
     return 0;
 }
