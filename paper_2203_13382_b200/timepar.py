@@ -43,12 +43,19 @@ from . import _lib
 
 
 class Comm:
-    """Neighbour shifts and all-gathers over a torch.distributed group."""
+    """Neighbour shifts and all-gathers over a torch.distributed group.
 
-    def __init__(self, group=None):
+    With NCCL the device rows move directly over NVLink.  ``host_staged``
+    routes them through host memory instead, which lets the gloo backend
+    drive the CUDA engine (used to test several ranks on one GPU)."""
+
+    def __init__(self, group=None, host_staged: bool | None = None):
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.size = dist.get_world_size(group) if dist.is_initialized() else 1
+        if host_staged is None:
+            host_staged = dist.is_initialized() and dist.get_backend(group) != "nccl"
+        self.host_staged = host_staged
 
     def _global(self, r):
         return dist.get_global_rank(self.group, r) if self.group is not None else r
@@ -59,17 +66,28 @@ class Comm:
             return
         ops = []
         dst, src = self.rank + direction, self.rank - direction
-        if send is not None and 0 <= dst < self.size:
-            ops.append(dist.P2POp(dist.isend, send, self._global(dst), self.group))
-        if recv is not None and 0 <= src < self.size:
-            ops.append(dist.P2POp(dist.irecv, recv, self._global(src), self.group))
+        has_send = send is not None and 0 <= dst < self.size
+        has_recv = recv is not None and 0 <= src < self.size
+        s_buf = send.cpu() if (has_send and self.host_staged and send.is_cuda) else send
+        r_buf = torch.empty_like(recv, device="cpu") if (has_recv and self.host_staged and recv.is_cuda) else recv
+        if has_send:
+            ops.append(dist.P2POp(dist.isend, s_buf, self._global(dst), self.group))
+        if has_recv:
+            ops.append(dist.P2POp(dist.irecv, r_buf, self._global(src), self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if has_recv and r_buf is not recv:
+            recv.copy_(r_buf)
 
     def allgather(self, full: torch.Tensor, local: torch.Tensor):
         if self.size == 1:
             full.copy_(local)
+            return
+        if self.host_staged and full.is_cuda:
+            parts = [torch.empty_like(local, device="cpu") for _ in range(self.size)]
+            dist.all_gather(parts, local.contiguous().cpu(), group=self.group)
+            full.copy_(torch.cat(parts).reshape(full.shape))
             return
         dist.all_gather_into_tensor(full, local.contiguous(), group=self.group)
 
