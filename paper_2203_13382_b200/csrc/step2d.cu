@@ -245,29 +245,14 @@ __global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
             }
         }
     };
-    // fused pass: body(i, ix, iy) updates node i and returns its contribution
-    // to this pass's reduction; per-warp-block partials go to the partial buffer
-    auto pass = [&](auto &&body) {
+    auto reduce_nodes = [&](auto &&val) {
         double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
         for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
-            const int64_t base = wb * kWB;
-            const int iy0 = row_blocks ? (int)(base / nx) : 0;
-            const int ix0 = row_blocks ? (int)(base - (int64_t)iy0 * nx) : 0;
             double acc = 0.0;
 #pragma unroll
             for (int k = 0; k < kWBPerLane; ++k) {
-                const int64_t i = base + lane + 32 * k;
-                if (i < n) {
-                    int ix, iy;
-                    if (row_blocks) {
-                        ix = ix0 + lane + 32 * k;
-                        iy = iy0;
-                    } else {
-                        iy = (int)((unsigned)i / (unsigned)nx);
-                        ix = (int)i - iy * nx;
-                    }
-                    acc = __dadd_rn(acc, body(i, ix, iy));
-                }
+                const int64_t i = wb * kWB + lane + 32 * k;
+                if (i < n) acc = __dadd_rn(acc, val(i));
             }
             acc = warp_sum(acc);
             if (lane == 0 && active_cta) pb[wb] = acc;
@@ -302,12 +287,12 @@ __global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
         int bad = 0;
         if (active) {
             const double *u = a.U_in + b * a.ld_in;
-            pass([&](int64_t i, int, int) {
+            for_nodes([&](int64_t i, int ix, int iy) {
                 const double v = sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
                 w[i] = v;
                 if (!isfinite(v)) bad = 1;
-                return __dmul_rn(v, v);
             });
+            reduce_nodes([&](int64_t i) { return __dmul_rn(w[i], w[i]); });
         }
         bad = __syncthreads_or(bad);
         if (active && tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
@@ -321,7 +306,7 @@ __global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
         if (active && anybad && tid == 0 && chunk == 0) atomicExch(C.status, 1);
         if (!skip) {
             const double yb = 1.0 / beta;
-            for_nodes([&](int64_t i, int, int) { basis[i] = div_rcp(w[i], beta, yb); });
+            for_nodes([&](int64_t i, int ix, int iy) { basis[i] = div_rcp(w[i], beta, yb); });
         }
         if (tid == 0) S.stop = skip ? 1 : 0;
         if (active_cta && tid == 0 && chunk == 0) C.stopflags[slot] = skip ? 1 : 0;
@@ -338,11 +323,10 @@ __global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
             const double *bk = basis + (int64_t)kk * n;
             // w = A b_kk ; inner product with b_0
             if (run) {
-                pass([&](int64_t i, int ix, int iy) {
-                    const double wi = imsd2d_at<P>(bk, nx, ix, iy, __ldg(gx + i), __ldg(gy + i));
-                    w[i] = wi;
-                    return __dmul_rn(basis[i], wi);
+                for_nodes([&](int64_t i, int ix, int iy) {
+                    w[i] = imsd2d_at<P>(bk, nx, ix, iy, __ldg(gx + i), __ldg(gy + i));
                 });
+                reduce_nodes([&](int64_t i) { return __dmul_rn(basis[i], w[i]); });
             }
             double hrun = 0.0;
             for (int j = 0; j <= kk; ++j) {
@@ -361,11 +345,8 @@ __global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
                 if (run) {
                     const double *bj = basis + (int64_t)j * n;
                     const double *bn = j < kk ? basis + (int64_t)(j + 1) * n : nullptr;
-                    pass([&](int64_t i, int, int) {
-                        const double wi = fma(-h, bj[i], w[i]);
-                        w[i] = wi;
-                        return __dmul_rn(bn ? bn[i] : wi, wi);
-                    });
+                    for_nodes([&](int64_t i, int ix, int iy) { w[i] = fma(-h, bj[i], w[i]); });
+                    reduce_nodes([&](int64_t i) { return __dmul_rn(bn ? bn[i] : w[i], w[i]); });
                 }
             }
             const double nrm = sqrt(gtotal());
@@ -374,7 +355,7 @@ __global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
                 if (!brk) {
                     const double yn = 1.0 / nrm;
                     double *bn = basis + (int64_t)(kk + 1) * n;
-                    for_nodes([&](int64_t i, int, int) { bn[i] = div_rcp(w[i], nrm, yn); });
+                    for_nodes([&](int64_t i, int ix, int iy) { bn[i] = div_rcp(w[i], nrm, yn); });
                 }
                 __syncthreads();
                 if (tid == 0) {
@@ -407,7 +388,7 @@ __global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
         }
         __syncthreads();
         if (active) {
-            pass([&](int64_t i, int, int) {
+            for_nodes([&](int64_t i, int ix, int iy) {
                 double x = 0.0;
                 if (anybad) {
                     x = __longlong_as_double(0x7ff8000000000000LL);
@@ -416,9 +397,10 @@ __global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
                 }
                 const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
                 x = a.U_sub ? __dsub_rn(__dadd_rn(g, x), a.U_sub[b * a.ld_sub + i]) : __dadd_rn(x, g);
+                w[i] = x;
                 if (a.out) a.out[b * a.ld_out + i] = x;
-                return __dmul_rn(x, x);
             });
+            reduce_nodes([&](int64_t i) { return __dmul_rn(w[i], w[i]); });
         }
         const double tot = gtotal();
         if (active && tid == 0 && chunk == 0) {
