@@ -175,7 +175,8 @@ def run_gpu(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    kw = CONFIGS[args.config]
+    kw = dict(CONFIGS[args.config], gmres_variant=args.gmres_variant)
+    P.set_launch_policy(args.launch_policy)
     cfg = P.SolverConfig(**kw)
     t0 = time.perf_counter()
     levels = P.build_hierarchy(cfg)
@@ -312,7 +313,8 @@ def run_gpu(args):
                        "dt": levels[0].dt, "parallelism": f"time-sharded over {world} GPUs (NCCL halo rows)" if world > 1 else "1gpu",
                        "l2": f"inputs larger than L2 (U {8 * (cfg.n_t + 1) * npts / 1e6:.0f} MB + fine records "
                              f"{8 * cfg.dim * cfg.n_t * npts / 1e6:.0f} MB > 126 MB)",
-                       "setup_s": round(setup_s, 4), "iterations": iters, "status": rep.status},
+                       "setup_s": round(setup_s, 4), "iterations": iters, "status": rep.status,
+                       "gmres_variant": cfg.gmres_variant, "launch_policy": args.launch_policy},
             "roofline": roofline,
             "sl_step_roofline": sl_roof,
             "cpu_baseline": cpu,
@@ -494,6 +496,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-samples", type=int, default=1)
+    ap.add_argument("--gmres-variant", default="mgs", choices=["mgs", "mgs_lowsync"],
+                    help="coarse-level Arnoldi orthogonalisation (mgs = the reference's loop)")
+    ap.add_argument("--launch-policy", default="auto", choices=["auto", "cta", "cluster"],
+                    help="corrected 1D kernels: one CTA or one 8-SM cluster per row chain")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     args = ap.parse_args()
     if args.warmup < 3:

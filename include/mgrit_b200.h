@@ -30,9 +30,12 @@
 extern "C" {
 #endif
 
-#define MGRIT_ABI_VERSION 1
+#define MGRIT_ABI_VERSION 2
 
 enum { MGRIT_OK = 0, MGRIT_EINVAL = 2, MGRIT_ECUDA = 3 };
+/* launch policy of corrected 1D phases / sweeps: AUTO picks the cluster-split
+ * kernels when the level has too few row chains to fill the GPU */
+enum { MGRIT_LAUNCH_AUTO = 0, MGRIT_LAUNCH_CTA = 1, MGRIT_LAUNCH_CLUSTER = 2 };
 
 /* operator kinds (mgrit.py:34).  MGRIT_KIND_SL covers "fine" and
  * "rediscretized" (plain semi-Lagrangian step); "ideal" is composed on the
@@ -65,6 +68,12 @@ typedef struct mgrit_level_desc {
     int32_t gmres_max_iters;/* GmresConfig.max_iters (coarse_correction.py:157-170) */
     int32_t stencil_numba;  /* 1: numba grouping of the D stencil sum (_kernels.py:18-31) */
     double gmres_tol;       /* < 0 : fixed iteration count (tol None) */
+    int32_t gmres_lowsync;  /* 0: classic MGS (the reference's loop, default);
+                               1: low-synchronisation MGS -- same coefficients in
+                               exact arithmetic, one block reduction per Arnoldi
+                               step instead of k+1 (1D only) */
+    int32_t launch_policy;  /* MGRIT_LAUNCH_*: corrected 1D levels may run one
+                               thread-block cluster (8 SMs) per row chain */
 } mgrit_level_desc;
 
 /* ERK tableau for departure tracing (semi_lagrangian.py:46-72); built on the

@@ -8,7 +8,7 @@ sm_100a kernels in libmgrit_b200.so (C ABI: include/mgrit_b200.h).
 from .core import (Grid1D, Grid2D, TimeGrid, WaveSpeed, get_wave_speed,  # noqa: F401
                    initial_condition, random_state, space_time_norm)
 from .mgrit import (ConvergenceReport, GmresConfig, Level, SolverConfig,  # noqa: F401
-                    build_hierarchy, c_relax, departures_from_coords, f_relax,
+                    build_hierarchy, c_relax, departures_from_coords, f_relax, set_launch_policy,
                     residual, sequential_reference, solve, solve_sequential,
                     v_cycle)
 

@@ -28,6 +28,7 @@ class LevelDesc(ctypes.Structure):
         ("shared", c_i32), ("n_steps", c_i32), ("n_points", c_i64),
         ("s_x", c_vp), ("s_y", c_vp), ("sig_x", c_vp), ("sig_y", c_vp),
         ("gmres_max_iters", c_i32), ("stencil_numba", c_i32), ("gmres_tol", c_dbl),
+        ("gmres_lowsync", c_i32), ("launch_policy", c_i32),
     ]
 
 
@@ -91,7 +92,7 @@ def load(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.mgrit_abi_version() != 1:
+    if lib.mgrit_abi_version() != 2:
         raise RuntimeError("libmgrit_b200.so ABI mismatch")
     if path is None:
         _LIB = lib

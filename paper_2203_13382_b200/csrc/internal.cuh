@@ -24,6 +24,10 @@ int sweep_1d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G,
              int zero_init, int32_t *gmres_iters, void *scratch, int64_t scratch_bytes,
              int32_t *status, cudaStream_t st);
 int64_t rows_capacity(const mgrit_level_desc *L);
+// cluster-split corrected 1D kernels; return -1 when not applicable
+int cl_level_phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int32_t *status, cudaStream_t st);
+int cl_sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg, int zero_init,
+             int32_t *gmres_iters, int32_t *status, cudaStream_t st);
 
 int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, int64_t scratch_bytes,
                   int32_t *status, cudaStream_t st);

@@ -39,6 +39,12 @@ int apply_rows_1d(const mgrit_level_desc *L, const RowsArgs &a, void *scratch,
 int level_phase_1d(const mgrit_level_desc *L, const mgrit_phase_args *A, void *scratch,
                    int64_t scratch_bytes, int32_t *status, cudaStream_t st) {
     if (int rc = validate(L)) return rc;
+    if (L->kind == MGRIT_KIND_CORRECTED && A && A->m >= 1 && A->U && A->Cbuf && A->n_intervals >= 1 &&
+        (int64_t)A->n_intervals * A->m == L->n_steps && A->phase >= 0 && A->phase <= 3 &&
+        (A->phase != MGRIT_PHASE_INJ_F || A->Uc)) {
+        const int rc = cl_level_phase(L, A, status, st);
+        if (rc >= 0) return rc;
+    }
     return dispatch_pk(L->p, L->kind, [&](auto X) {
         return decltype(X)::phase(L, A, scratch, scratch_bytes, status, st);
     });
@@ -48,6 +54,10 @@ int sweep_1d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G,
              int zero_init, int32_t *gmres_iters, void *scratch, int64_t scratch_bytes,
              int32_t *status, cudaStream_t st) {
     if (int rc = validate(L)) return rc;
+    if (L->kind == MGRIT_KIND_CORRECTED && U) {
+        const int rc = cl_sweep(L, U, ldu, G, ldg, zero_init, gmres_iters, status, st);
+        if (rc >= 0) return rc;
+    }
     return dispatch_pk(L->p, L->kind, [&](auto X) {
         return decltype(X)::sweep(L, U, ldu, G, ldg, zero_init, gmres_iters, scratch,
                                   scratch_bytes, status, st);

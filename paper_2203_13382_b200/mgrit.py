@@ -35,16 +35,39 @@ _KIND_CODE = {"fine": _lib.KIND_SL, "rediscretized": _lib.KIND_SL, "corrected": 
               "forward_euler": _lib.KIND_FORWARD_EULER}
 
 
+GMRES_VARIANTS = ("mgs", "mgs_lowsync")
+LAUNCH_POLICIES = {"auto": 0, "cta": 1, "cluster": 2}
+_launch_policy = "auto"
+
+
+def set_launch_policy(policy: str) -> str:
+    """Kernel shape of corrected 1D phases/sweeps: "auto" (cluster-split when a
+    level has too few row chains to fill the GPU), "cta" (one CTA per row
+    chain) or "cluster" (8-CTA cluster per row chain whenever eligible).
+    Returns the previous policy."""
+    global _launch_policy
+    if policy not in LAUNCH_POLICIES:
+        raise ValueError(f"launch policy must be one of {sorted(LAUNCH_POLICIES)}")
+    prev, _launch_policy = _launch_policy, policy
+    return prev
+
+
 @dataclass(frozen=True)
 class GmresConfig:
     """coarse_correction.py:157-170 — tol None runs exactly max_iters iterations."""
 
     max_iters: int = 10
     tol: float | None = None
+    # "mgs": the reference's modified Gram-Schmidt loop; "mgs_lowsync": the
+    # same projection coefficients via one fused reduction per Arnoldi step
+    # (Gram-corrected, 1D levels only) -- equal in exact arithmetic, not bitwise
+    variant: str = "mgs"
 
     def __post_init__(self):
         if self.max_iters < 1:
             raise ValueError("max_iters must be at least 1")
+        if self.variant not in GMRES_VARIANTS:
+            raise ValueError(f"gmres variant must be one of {GMRES_VARIANTS}")
 
 
 @dataclass(frozen=True)
@@ -64,6 +87,7 @@ class SolverConfig:
     operator_kind: str = "corrected"
     departure_policy: str = "backtrack"
     gmres_mode: str | None = None
+    gmres_variant: str = "mgs"
     relaxation: str = "FCF"
     seed: int = 0
     rtol: float = 1e-10
@@ -85,6 +109,8 @@ class SolverConfig:
             raise ValueError("relaxation must be 'FCF' or 'F'")
         if self.gmres_mode not in (None, "fixed", "tolerance"):
             raise ValueError("gmres_mode must be 'fixed', 'tolerance', or None")
+        if self.gmres_variant not in GMRES_VARIANTS:
+            raise ValueError(f"gmres_variant must be one of {GMRES_VARIANTS}")
         if self.u0 not in ("reference", "sin4"):
             raise ValueError("u0 must be 'reference' or 'sin4'")
         if self.iterate not in ("uniform01", "pm1"):
@@ -199,6 +225,8 @@ class Level:
         d.gmres_max_iters = g.max_iters
         d.gmres_tol = -1.0 if g.tol is None else float(g.tol)
         d.stencil_numba = int(self.stencil_numba if stencil_numba is None else stencil_numba)
+        d.gmres_lowsync = int(g.variant == "mgs_lowsync" and self.grid.dim == 1)
+        d.launch_policy = LAUNCH_POLICIES[_launch_policy]
         return d
 
     @property
@@ -398,7 +426,7 @@ def build_hierarchy(cfg: SolverConfig, fine_coords=None, keep_displacements: boo
     if not keep_displacements:
         levels[-1].disp_x = levels[-1].disp_y = None
     mode = cfg.gmres_mode or ("fixed" if len(levels) == 2 else "tolerance")
-    gcfg = GmresConfig(10, None) if mode == "fixed" else GmresConfig(10, 1e-2)
+    gcfg = GmresConfig(10, None if mode == "fixed" else 1e-2, cfg.gmres_variant)
     for lvl in levels[1:]:
         lvl.gmres_cfg = gcfg
     # the reference's numba sweep (mgrit.py:304-305) groups the D-stencil sum
@@ -742,7 +770,8 @@ class _Session:
 
 
 def _session(levels, cfg, dev) -> _Session:
-    key = (cfg.n_t, cfg.relaxation, tuple((lv.kind, lv.gmres_cfg, lv.stencil_numba) for lv in levels))
+    key = (cfg.n_t, cfg.relaxation, _launch_policy,
+           tuple((lv.kind, lv.gmres_cfg, lv.stencil_numba) for lv in levels))
     cache = levels[0].__dict__.setdefault("_sessions", {})
     sess = cache.get(key)
     if sess is None:

@@ -190,6 +190,33 @@ def test_corrected_step_matches_oracle(P, p, mode):
         assert list(_np(iters)) == log.counts
 
 
+@pytest.mark.parametrize("p", [1, 3, 5])
+@pytest.mark.parametrize("mode", ["fixed", "tolerance"])
+@pytest.mark.parametrize("n_x", [128, 4096])
+def test_corrected_step_lowsync_matches_oracle(P, p, mode, n_x):
+    """Low-synchronisation MGS: the reference's GMRES result and Arnoldi counts
+    (equal in exact arithmetic; relative 1e-12 in fp64)."""
+    kw = dict(n_x=n_x, n_t=64, wave_speed="C3", p=p, schedule=4, gmres_mode=mode)
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, olevels = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    rng = np.random.default_rng(12)
+    for li in (1, 2):
+        lv, ol = levels[li], olevels[li]
+        lv.gmres_cfg = P.GmresConfig(lv.gmres_cfg.max_iters, lv.gmres_cfg.tol, "mgs_lowsync")
+        U = rng.standard_normal((lv.n_steps, n_x))
+        t = np.arange(lv.n_steps)
+        log = O.GmresLog()
+        ol.log = log
+        want = ol.step_batch(t, U)
+        iters = torch.zeros(lv.n_steps, dtype=torch.int32, device=dev())
+        out = torch.empty((lv.n_steps, n_x), dtype=torch.float64, device=dev())
+        lv._apply(torch.from_numpy(U).to(dev()), 0, 0, lv.n_steps, out,
+                  t_idx=torch.arange(lv.n_steps, device=dev()), gmres_iters=iters)
+        assert _rel(_np(out), want) < 1e-12
+        assert list(_np(iters)) == log.counts
+
+
 def test_forward_euler_and_ideal_levels(P):
     for kind in ("forward_euler", "ideal"):
         kw = dict(n_x=64, n_t=64, wave_speed="C3", p=3, schedule=4, operator_kind=kind, max_levels=2)
@@ -271,6 +298,30 @@ def test_solve_2d_matches_reference_golden(P, golden_index, name):
     g = load_solve(name)
     rep, U = P.solve(P.SolverConfig(**info["kw"]))
     _check_solve(rep, U, info, g, exact_records=False, name=name)
+
+
+LOWSYNC_1D = ["tiny1d_C3_p3_m4", "tiny1d_B2_p5_m8", "tiny1d_C1_2lvl_pm1", "kind_F_relax", "kind_ideal",
+              "kind_schedule_16_4", "crit1_C1_p1_m16", "crit1_C1_p5_m4", "crit1_C3_p5_m16", "crit2_C1_p3_m4",
+              "crit2_C3_p5_m16", "cfg1_full", "cfg1_085h", "cfg3_reduced"]
+
+
+@pytest.mark.parametrize("name", LOWSYNC_1D)
+def test_solve_lowsync_matches_reference_golden(P, golden_index, name):
+    """gmres_variant="mgs_lowsync": same iteration counts and histories as the
+    reference (1e-12 r0), iterates relative 1e-12."""
+    info = golden_index[name]
+    g = load_solve(name)
+    rep, U = P.solve(P.SolverConfig(**info["kw"], gmres_variant="mgs_lowsync"))
+    _check_solve(rep, U, info, g, exact_records=False, name=name)
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_lowsync_matches_reference(P, golden_index):
+    info = golden_index["cfg2_full"]
+    g = load_solve("cfg2_full")
+    rep, U = P.solve(P.SolverConfig(**info["kw"], gmres_variant="mgs_lowsync"))
+    _check_solve(rep, U, info, g, exact_records=False)
+    assert np.allclose(np.linalg.norm(U, axis=1), g["row_norms"], rtol=1e-12, atol=0)
 
 
 @pytest.mark.slow
@@ -484,3 +535,87 @@ def test_cli_run_report_matches_reference_format(P, tmp_path, golden_index):
     assert rep["iterations"] == golden_index["tiny1d_C3_p3_m4"]["iterations"]
     assert np.allclose(rep["residual_norms"], g["hist"], rtol=0, atol=1e-12 * g["hist"][0])
     assert open(out + ".csv").readline().strip() == "iteration,residual_norm"
+
+
+# ---------------------------------------------------------------------------
+# cluster-split corrected kernels (one 8-CTA cluster per row chain)
+
+
+@pytest.fixture
+def cluster_policy(P):
+    prev = P.set_launch_policy("cluster")
+    yield
+    P.set_launch_policy(prev)
+
+
+@pytest.mark.parametrize("variant", ["mgs", "mgs_lowsync"])
+@pytest.mark.parametrize("name", ["cfg1_full", "cfg1_085h", "cfg3_reduced"])
+def test_solve_cluster_matches_reference_golden(P, golden_index, cluster_policy, name, variant):
+    """Corrected phases and the coarsest sweep on 8-SM clusters (DSMEM
+    all-reduces, TMA-multicast rows): reference iteration counts and
+    histories within 1e-12 r0."""
+    info = golden_index[name]
+    g = load_solve(name)
+    rep, U = P.solve(P.SolverConfig(**info["kw"], gmres_variant=variant))
+    _check_solve(rep, U, info, g, exact_records=False, name=name)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("variant", ["mgs", "mgs_lowsync"])
+def test_cfg2_full_size_cluster_matches_reference(P, golden_index, cluster_policy, variant):
+    info = golden_index["cfg2_full"]
+    g = load_solve("cfg2_full")
+    rep, U = P.solve(P.SolverConfig(**info["kw"], gmres_variant=variant))
+    _check_solve(rep, U, info, g, exact_records=False)
+    assert np.allclose(np.linalg.norm(U, axis=1), g["row_norms"], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("variant", ["mgs", "mgs_lowsync"])
+@pytest.mark.parametrize("n_x,p,speed,m,levels", [(1024, 1, "C1", 4, None), (2048, 3, "C3", 4, None),
+                                                  (4096, 5, "B2", 8, None), (8192, 3, "C2", 4, 2),
+                                                  (2048, 5, "C3", 16, 2)])
+def test_cluster_solve_matches_oracle(P, cluster_policy, n_x, p, speed, m, levels, variant):
+    """Every cluster configuration (n = 1024 .. 8192, p = 1/3/5, two-level
+    fixed-K and multilevel tolerance GMRES) against the oracle."""
+    kw = dict(n_x=n_x, n_t=64, wave_speed=speed, p=p, schedule=m, max_levels=levels, seed=3,
+              max_iters=5, rtol=0.0)
+    cfg, ocfg = _cfg_pair(P, kw)
+    cfg = P.SolverConfig(**kw, gmres_variant=variant)
+    coords, olevels = _fine_coords(ocfg)
+    lv = P.build_hierarchy(cfg, fine_coords=coords)
+    rep, U = P.solve(cfg, lv)
+    orep, oU = O.solve(ocfg, olevels)
+    r0 = orep.residual_norms[0]
+    assert rep.iterations == orep.iterations
+    assert np.all(np.abs(rep.residual_norms - orep.residual_norms) <= 1e-12 * r0)
+    assert _rel(U, oU) <= U_TOL
+
+
+def test_cluster_sweep_counts_match_oracle(P, cluster_policy):
+    """Coarsest sequential sweep on one cluster: rows and per-step Arnoldi
+    counts equal the oracle's sweep (numba grouping, >= 64 steps)."""
+    kw = dict(n_x=1024, n_t=256, wave_speed="C3", p=3, schedule=4, max_levels=2)
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, olevels = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    rng = np.random.default_rng(5)
+    G = rng.standard_normal((levels[1].n_steps + 1, 1024))
+    Uo = np.zeros_like(G)
+    Uo[0] = rng.standard_normal(1024)
+    Ud = torch.from_numpy(Uo.copy()).to(dev())
+    log = O.GmresLog()
+    olevels[1].log = log
+    O.solve_sequential(olevels[1], Uo, G)
+    import ctypes
+    from paper_2203_13382_b200 import _lib
+    lib = _lib.load()
+    d = levels[1].desc(stencil_numba=True)
+    Gd = torch.from_numpy(G).to(dev())
+    iters = torch.zeros(levels[1].n_steps, dtype=torch.int32, device=dev())
+    status = torch.zeros(1, dtype=torch.int32, device=dev())
+    rc = lib.mgrit_sequential_sweep(ctypes.byref(d), Ud.data_ptr(), 1024, Gd.data_ptr(), 1024, 0,
+                                    iters.data_ptr(), None, 0, status.data_ptr(), None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert _rel(_np(Ud), Uo) < 1e-12
+    assert list(_np(iters)) == log.counts

@@ -38,6 +38,7 @@ int main(int argc, char **argv) {
     mgrit_level_desc L{};
     L.dim = 1; L.n_x = n; L.p = 3; L.kind = MGRIT_KIND_CORRECTED; L.shared = 1; L.n_steps = 1; L.n_points = n;
     L.s_x = ds; L.sig_x = dsig; L.gmres_max_iters = K; L.gmres_tol = -1.0;
+    L.gmres_lowsync = argc > 3 ? atoi(argv[3]) : 0;
     RowsArgs a{1, nullptr, 0, 0, du, n, nullptr, n, nullptr, n, dout, n, nullptr, nullptr};
     for (int rep = 0; rep < 3; ++rep)
         Launch1D<3, MGRIT_KIND_CORRECTED>::rows(&L, a, scr, (int64_t)(K + 1) * n * 8, st, 0);
@@ -52,7 +53,10 @@ int main(int argc, char **argv) {
                q[6] - q[5], q[6] - q[0]);
     }
     printf(" xcomb %lld   total %lld cycles\n", h[201] - h[200], h[201] - h[0]);
-    if (K > 5)
+    if (K > 5 && L.gmres_lowsync)
+        printf("  kk=5 lowsync: passA %lld  bar %lld  warp0 %lld  bar %lld  passB %lld\n", h[302] - h[301],
+               h[303] - h[302], h[304] - h[303], h[305] - h[304], h[306] - h[305]);
+    else if (K > 5)
         for (int j = 0; j <= 5; ++j) {
             long long *q = h + 300 + 4 * j;
             printf("  kk=5 j=%d: dot->prefetch-issued %lld, prefetch->h %lld (reduction), h->axpy-done %lld, next-dot %lld\n",
