@@ -480,6 +480,8 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
                 __syncwarp();
                 const double d = lane <= kk ? tot : 0.0;
                 double hh = d;
+                // Gram row of this lane (branch-free: clamped row, masked use)
+                const double *grow_l = S.gram + (lane <= kk ? lane : 0) * kMaxKrylov;
                 if (gmax <= 1e-9) {
                     // |G_ij| <= 1e-9: the second-order term of (I + L)^{-1} d
                     // is below 2.3e-16 |h| (|L| <= 15e-9), under the rounding
@@ -487,13 +489,15 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
 #pragma unroll
                     for (int i = 0; i < kk; ++i) {
                         const double di = __shfl_sync(0xffffffffu, d, i);
-                        if (i < lane && lane <= kk) hh = fma(-S.gram[lane * kMaxKrylov + i], di, hh);
+                        const double gi = grow_l[i];
+                        hh = (i < lane && lane <= kk) ? fma(-gi, di, hh) : hh;
                     }
                 } else {
 #pragma unroll
                     for (int i = 0; i < kk; ++i) {
                         const double hi = __shfl_sync(0xffffffffu, hh, i);
-                        if (i < lane && lane <= kk) hh = fma(-S.gram[lane * kMaxKrylov + i], hi, hh);
+                        const double gi = grow_l[i];
+                        hh = (i < lane && lane <= kk) ? fma(-gi, hi, hh) : hh;
                     }
                 }
                 if (lane <= kk) S.hv[lane] = hh;
@@ -563,6 +567,7 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
         if (brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta))) break;
     }
     __syncthreads();  // S.H / S.g / S.rdiag from thread 0
+    MGRIT_PROBE_AT(482);
     // back substitution (warp 0; y_j = acc / H_jj via the stored reciprocal,
     // correctly rounded) and x = sum_j b_j y_j on the chunk
     if (tid < 32) {
@@ -570,28 +575,33 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
         double acc = lane < done ? S.g[lane] : 0.0;
         const double hjj = lane < done ? S.H[lane * kMaxKrylov + lane] : 1.0;
         const double rjj = lane < done ? S.rdiag[lane] : 1.0;
+        // branch-free: steps j >= done give y_j = 0 / 1 = 0 and touch nothing
         double myy = 0.0;
 #pragma unroll
         for (int j = KM - 1; j >= 0; --j) {
-            if (j < done) {
-                const double yj = __shfl_sync(0xffffffffu, div_rcp(acc, hjj, rjj), j);
-                myy = lane == j ? yj : myy;
-                const double hlj = lane < j ? S.H[lane * kMaxKrylov + j] : 0.0;
-                acc = lane < j ? __dsub_rn(acc, __dmul_rn(hlj, yj)) : acc;
-            }
+            const double yj = __shfl_sync(0xffffffffu, div_rcp(acc, hjj, rjj), j);
+            myy = lane == j ? yj : myy;
+            const bool upd = lane < j && j < done;
+            const double hlj = upd ? S.H[lane * kMaxKrylov + j] : 0.0;
+            acc = upd ? __dsub_rn(acc, __dmul_rn(hlj, yj)) : acc;
         }
-        if (lane < done) S.y[lane] = myy;
+        if (lane < KM) S.y[lane] = myy;
     }
+    MGRIT_PROBE_AT(483);
     __syncthreads();
+    MGRIT_PROBE_AT(484);
 #pragma unroll
     for (int k = 0; k < NPT; ++k) v[k] = 0.0;
+    // branch-free (slots j >= done may hold stale values: masked loads)
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
-        if (j < done) {
-            const double yj = S.y[j];
-            const double *bj = cx.slot(j);
+        const bool use = j < done;
+        const double yj = S.y[j];
+        const double *bj = cx.slot(j);
 #pragma unroll
-            for (int k = 0; k < NPT; ++k) v[k] = fma(bj[tid + k * NTC], yj, v[k]);
+        for (int k = 0; k < NPT; ++k) {
+            const double b = use ? bj[tid + k * NTC] : 0.0;
+            v[k] = fma(b, yj, v[k]);
         }
     }
     MGRIT_PROBE_AT(481);

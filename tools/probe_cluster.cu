@@ -22,7 +22,8 @@ int main(int argc, char **argv) {
     const int n = argc > 1 ? atoi(argv[1]) : 4096;
     const int K = argc > 2 ? atoi(argv[2]) : 10;
     const int lowsync = argc > 3 ? atoi(argv[3]) : 0;
-    std::vector<double> s(n), sig(n), u(2 * n, 0.0);
+    const int steps = argc > 4 ? atoi(argv[4]) : 1;
+    std::vector<double> s(n), sig(n), u((steps + 1) * n, 0.0);
     srand(1);
     for (int i = 0; i < n; ++i) {
         s[i] = i + 0.37 + 0.2 * (rand() / (double)RAND_MAX);
@@ -32,15 +33,15 @@ int main(int argc, char **argv) {
     }
     double *ds, *dsig, *du;
     int *st;
-    cudaMalloc(&ds, n * 8); cudaMalloc(&dsig, n * 8); cudaMalloc(&du, 2 * n * 8);
+    cudaMalloc(&ds, n * 8); cudaMalloc(&dsig, n * 8); cudaMalloc(&du, (steps + 1) * n * 8);
     cudaMalloc(&st, 4); cudaMemset(st, 0, 4);
     cudaMemcpy(ds, s.data(), n * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(dsig, sig.data(), n * 8, cudaMemcpyHostToDevice);
     mgrit_level_desc L{};
-    L.dim = 1; L.n_x = n; L.p = 3; L.kind = MGRIT_KIND_CORRECTED; L.shared = 1; L.n_steps = 1; L.n_points = n;
+    L.dim = 1; L.n_x = n; L.p = 3; L.kind = MGRIT_KIND_CORRECTED; L.shared = 1; L.n_steps = steps; L.n_points = n;
     L.s_x = ds; L.sig_x = dsig; L.gmres_max_iters = K; L.gmres_tol = -1.0; L.gmres_lowsync = lowsync;
     for (int rep = 0; rep < 3; ++rep) {
-        cudaMemcpy(du, u.data(), 2 * n * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(du, u.data(), (steps + 1) * n * 8, cudaMemcpyHostToDevice);
         int rc = cl::LaunchCl<3>::sweep(&L, du, n, nullptr, 0, 0, nullptr, st, 0);
         if (rc) { printf("launch rc %d\n", rc); return 1; }
     }
@@ -48,13 +49,15 @@ int main(int argc, char **argv) {
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
     long long h[512];
     cudaMemcpyFromSymbol(h, g_probe, sizeof(h));
-    printf("n=%d K=%d lowsync=%d  await_row %lld  SL+sig %lld  beta %lld  b0 %lld\n", n, K, lowsync, h[401] - h[400],
+    printf("n=%d K=%d lowsync=%d steps=%d  await_row %lld  SL+sig %lld  beta %lld  b0 %lld\n", n, K, lowsync, steps, h[401] - h[400],
            h[402] - h[401], h[403] - h[402], h[404] - h[403]);
     for (int kk = 0; kk < K; ++kk) {
         long long *q = h + 410 + 6 * kk;
         printf(" kk=%d stencil %5lld  project %6lld  norm %5lld  normalize %5lld  givens+sync %5lld  total %6lld\n", kk,
                q[1] - q[0], q[2] - q[1], q[3] - q[2], q[4] - q[3], q[5] - q[4], q[5] - q[0]);
     }
+    printf(" after-loop sync %lld  backsub %lld  sync %lld  xcomb %lld\n", h[482] - h[410 + 6 * (K - 1) + 5],
+           h[483] - h[482], h[484] - h[483], h[481] - h[484]);
     printf(" backsub+xcomb %lld   total %lld cycles\n", h[481] - h[410 + 6 * (K - 1) + 5], h[481] - h[400]);
     return 0;
 }
