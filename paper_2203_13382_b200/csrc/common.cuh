@@ -177,16 +177,6 @@ __device__ __forceinline__ double cmul(int idx, double x) {
 }
 
 // ---------------------------------------------------------------------------
-// cp.async (LDGSTS) staging of one fp64 per thread into shared memory
-
-__device__ __forceinline__ void cp_async8(double *smem_dst, const double *gmem_src) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-// ---------------------------------------------------------------------------
 // deterministic reductions
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -590,38 +590,20 @@ template <int P, int KIND, int NT, int NPT, bool F>
 __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_phase_args A, int nbs,
                                                    double *scratch, int32_t *status) {
     extern __shared__ double sm[];
-    // plain SL: the next step's departure records are staged into shared
-    // memory with cp.async while the current step computes (each thread
-    // stages and later reads only its own nodes, so no barrier is needed);
-    // other kinds prefetch into registers
-    constexpr bool ASYNC = KIND == MGRIT_KIND_SL && NPT <= 8;
-    constexpr bool PREFETCH = !ASYNC && NPT <= 8;
+    // The next step's departure records are prefetched into registers while
+    // the current step computes (plain SL and small NPT; register prefetch
+    // measured faster than cp.async staging through shared memory: the SL
+    // step is MIO-throttled and staging costs an LDGSTS plus an LDS per node).
+    // Plain SL rows up to 8192 nodes are double-buffered, so each step needs
+    // one barrier (write the other buffer, sync, swap) instead of two.
+    constexpr bool DBUF = KIND == MGRIT_KIND_SL && NPT <= 8;
+    constexpr bool PREFETCH = NPT <= 8;
     const int n = L.n_x;
     const int m = A.m;
     RowCtx cx = make_ctx(sm, n, nbs, scratch, blockIdx.x, L, status);
-    double *recbuf = cx.bsm;  // n doubles (ASYNC only)
-    // ASYNC (plain SL): the row is double-buffered, so each step needs one
-    // barrier (write the other buffer, sync, swap) instead of two.
-    // layout after GmresSmem: [recbuf n][halo | rowB n | halo]
+    // layout after GmresSmem: [halo | rowB n | halo]
     double *const rowA = cx.rowbuf;
-    double *const rowB = cx.bsm + n + kHalo;
-    auto stage = [&](int64_t t) {
-        const double *s = L.s_x + (L.shared ? 0 : t) * (int64_t)n;
-#pragma unroll
-        for (int k = 0; k < NPT; ++k) {
-            const int i = threadIdx.x + k * NT;
-            if (F || i < n) cp_async8(recbuf + i, s + i);
-        }
-        cp_async_commit();
-    };
-    auto take = [&](double (&sv)[NPT]) {
-        cp_async_wait_all();
-#pragma unroll
-        for (int k = 0; k < NPT; ++k) {
-            const int i = threadIdx.x + k * NT;
-            sv[k] = (F || i < n) ? recbuf[i] : 0.0;
-        }
-    };
+    double *const rowB = cx.bsm + kHalo;
     auto U = [&](int64_t t) { return A.U + (t - A.u_row0) * A.ldu; };
     auto Gr = [&](int64_t t) -> const double * { return A.G ? A.G + (t - A.g_row0) * A.ldg : nullptr; };
     auto Cb = [&](int64_t c) { return A.Cbuf + (c - A.c_row0) * (int64_t)n; };
@@ -631,8 +613,7 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
         const int64_t t0 = c * m;
         const int64_t tC = t0 + m;
         double v[NPT], sv[NPT];
-        if constexpr (ASYNC) stage(t0);
-        else load_records<NT, NPT, F>(L, t0, sv);
+        load_records<NT, NPT, F>(L, t0, sv);
         // ---- left state of the interval
         const bool zero_left = A.zero_init && (c == 0 || A.phase == MGRIT_PHASE_FC ||
                                                A.phase == MGRIT_PHASE_FONLY_RES);
@@ -655,7 +636,7 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
         } else if (A.phase == MGRIT_PHASE_F_RES && c > 0) {
             store_row<NT, NPT, F>(U(t0), v, n);
         }
-        if constexpr (ASYNC) cx.rowbuf = rowA;
+        if constexpr (DBUF) cx.rowbuf = rowA;
         set_row<NT, NPT, F>(cx.rowbuf, v, n);
 
         // ---- F-relaxation chain (mgrit.py:276-283) then the interval tail at
@@ -676,23 +657,20 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
         for (int k = 1; k <= kmax; ++k) {
             const int64_t t = t0 + k;
             double sn[PREFETCH ? NPT : 1];
-            if constexpr (ASYNC) {
-                take(sv);
-                if (k < kmax) stage(t);
-            } else if constexpr (PREFETCH) {
+            if constexpr (PREFETCH) {
                 if (k < kmax) load_records<NT, NPT, F>(L, t, sn);
             }
             cta_apply<P, KIND, NT, NPT, F, false>(L, t - 1, cx, v, sv);
             if constexpr (PREFETCH) {
 #pragma unroll
                 for (int q = 0; q < NPT; ++q) sv[q] = sn[q];
-            } else if constexpr (!ASYNC) {
+            } else {
                 if (k < kmax) load_records<NT, NPT, F>(L, t, sv);
             }
             if (k < m) {
                 add_forcing<NT, NPT, F>(v, Gr(t), n);
                 store_row<NT, NPT, F>(U(t), v, n);
-                if constexpr (ASYNC) {
+                if constexpr (DBUF) {
                     double *other = cx.rowbuf == rowB ? rowA : rowB;
 #pragma unroll
                     for (int q = 0; q < NPT; ++q) {
@@ -825,9 +803,9 @@ inline int max_smem_optin() {
 
 // Krylov slots that fit in shared memory next to the row
 inline int smem_slots(const mgrit_level_desc *L) {
-    // plain SL: cp.async record staging buffer + second row buffer (its halo
-    // comes from the 2*kHalo spare doubles smem_bytes_for always reserves)
-    if (L->kind == MGRIT_KIND_SL) return L->n_x <= 8192 ? 2 : 0;
+    // plain SL: second row buffer (its halo comes from the 2*kHalo spare
+    // doubles smem_bytes_for always reserves)
+    if (L->kind == MGRIT_KIND_SL) return L->n_x <= 8192 ? 1 : 0;
     if (L->kind != MGRIT_KIND_CORRECTED) return 0;
     const int64_t base = (int64_t)smem_bytes_for(L->n_x, 0);
     const int64_t avail = (int64_t)max_smem_optin() - base - 1024;
@@ -881,7 +859,7 @@ static int dispatch_cfg(Cfg1D, int n, Fn &&f) {
     } else {
         if (n == 1024) return f(Tag<P, KIND, 256, 4, true>{});
         if (n == 2048) return f(Tag<P, KIND, 256, 8, true>{});
-        if (n == 4096) return f(Tag<P, KIND, 512, 8, true>{});
+        if (n == 4096) return f(Tag<P, KIND, 1024, 4, true>{});
         if (n == 8192) return f(Tag<P, KIND, 1024, 8, true>{});
         if (n == 16384) return f(Tag<P, KIND, 1024, 16, true>{});
     }
