@@ -22,10 +22,17 @@ int by_p(int p, F &&f) {
     }
 }
 
-// A one-CTA corrected step costs about 1.7x a cluster step (B200, n = 4096,
-// cfg2 levels 3-5: 0.167 vs 0.096 ms per FC phase); pick the cluster kernels
-// when their wave count is below 1.7x the one-CTA kernel's.
-constexpr int64_t kCtaOverCluster10 = 17;
+// Cost of a wave of one-CTA corrected steps over a wave of cluster steps
+// (x10), measured on B200 per row length: n = 4096 (cfg2 levels 2-5: 0.167 vs
+// 0.096 ms per FC phase) and n = 16384 (cfg3 levels 1-3: 0.745 vs 0.142 ms
+// per wave); the shorter rows are extrapolated.  Cluster kernels are picked
+// when their wave count is below that multiple of the one-CTA kernel's.
+int64_t cta_over_cluster10(int n) {
+    if (n <= 2048) return 15;
+    if (n <= 4096) return 17;
+    if (n <= 8192) return 30;
+    return 50;
+}
 
 }  // namespace
 
@@ -40,7 +47,7 @@ int cl_level_phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int32_t
         const int64_t res_cta = rows_capacity(L);
         const int64_t waves_cta = (A->c_count + res_cta - 1) / (res_cta > 0 ? res_cta : 1);
         const int64_t waves_cl = (A->c_count + res_cl - 1) / res_cl;
-        if (10 * waves_cl >= kCtaOverCluster10 * waves_cta) return -1;
+        if (10 * waves_cl >= cta_over_cluster10(L->n_x) * waves_cta) return -1;
     }
     return by_p(L->p, [&](auto X) { return decltype(X)::phase(L, A, status, st, res_cl); });
 }

@@ -103,6 +103,8 @@ struct __align__(16) ClSmem {
 struct ClCtx {
     ClSmem *S;
     double *row;     // full state row (global node index), halo kHalo each side
+    const double *grow;  // GG (rows too large for shared memory): the global row
+    bool zrow;           // GG: the current row is all zeros
     double *slots;   // Krylov chunks: slot j interior at slots + j*ld + kHalo
     int ld;          // chunk + 2*kHalo
     int n, chunk;
@@ -113,9 +115,14 @@ struct ClCtx {
     __device__ double *slot(int j) const { return slots + j * ld + kHalo; }
 };
 
+// GG ("global gather"): rows too large for a shared-memory copy next to the
+// Krylov chunks (n = 16384) are gathered straight from L2; publication is
+// then a cluster barrier (release / acquire) instead of a TMA multicast.
+__host__ __device__ inline bool cl_gg(int n) { return n > 8192; }
+
 __host__ __device__ inline size_t cl_smem_bytes(int n, int K) {
     const int chunk = n / CS;
-    return sizeof(ClSmem) + sizeof(double) * ((size_t)n + 2 * kHalo) +
+    return sizeof(ClSmem) + (cl_gg(n) ? 0 : sizeof(double) * ((size_t)n + 2 * kHalo)) +
            sizeof(double) * (size_t)(K + 1) * (chunk + 2 * kHalo);
 }
 
@@ -124,9 +131,11 @@ __device__ __forceinline__ ClCtx make_clctx(int n, int K, int32_t *status) {
     ClCtx c;
     c.S = reinterpret_cast<ClSmem *>(clsm);
     c.row = reinterpret_cast<double *>(clsm + sizeof(ClSmem)) + kHalo;
+    c.grow = nullptr;
+    c.zrow = false;
     c.chunk = n / CS;
     c.ld = c.chunk + 2 * kHalo;
-    c.slots = c.row + n + kHalo;
+    c.slots = cl_gg(n) ? c.row - kHalo : c.row + n + kHalo;
     c.n = n;
     c.rank = ctarank();
     c.base = c.rank * c.chunk;
@@ -284,8 +293,16 @@ __device__ __forceinline__ double ar_multi(ClCtx &cx, double (&x)[V]) {
 // ------------------------------------------------------- row publication --
 // Every CTA multicasts its own chunk of `src` (a global row it has stored, or
 // that an earlier kernel wrote) into the full-row buffer of all CTAs; rank 0
-// and rank CS-1 also supply the periodic halos.
+// and rank CS-1 also supply the periodic halos.  GG: the chunk stores are
+// released with a cluster-barrier arrive; await_row is the acquire wait.
+template <bool GG>
 __device__ __forceinline__ void publish_row(ClCtx &cx, const double *src) {
+    if constexpr (GG) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        cx.grow = src;
+        cx.zrow = false;
+        return;
+    }
     fence_async_global();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -298,12 +315,22 @@ __device__ __forceinline__ void publish_row(ClCtx &cx, const double *src) {
         if (cx.rank == CS - 1) bulk_multicast(su32(cx.row - kHalo), src + cx.n - kHalo, kHalo * 8, bar, mask);
     }
 }
+template <bool GG>
 __device__ __forceinline__ void await_row(ClCtx &cx) {
+    if constexpr (GG) {
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
     mbar_wait(&cx.S->rowbar, cx.pubs & 1);
     ++cx.pubs;
 }
 // local all-zero row (no publication)
+template <bool GG>
 __device__ __forceinline__ void zero_row(ClCtx &cx) {
+    if constexpr (GG) {
+        cx.zrow = true;
+        return;
+    }
     __syncthreads();
     for (int i = threadIdx.x - kHalo; i < cx.n + kHalo; i += NTC) cx.row[i] = 0.0;
     __syncthreads();
@@ -342,7 +369,7 @@ constexpr int kMaxKrylovCl = 10;
 // v (chunk) = Phi_t(row): SL gather from the full row, then GMRES on
 // (I - diag(sig) D) x = v with the cluster reductions above.  Returns the
 // Arnoldi count (-1 on a non-finite right-hand side).
-template <int P, int NPT, bool NUMBA, bool LOWSYNC>
+template <int P, int NPT, bool NUMBA, bool LOWSYNC, bool GG>
 __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double (&v)[NPT],
                         const double (&sv)[NPT], bool wait_row) {
     constexpr int SLW = Stencil<P>::L;
@@ -352,27 +379,45 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
     ClSmem &S = *cx.S;
     // ---- semi-Lagrangian gather (same arithmetic as cta_apply)
     MGRIT_PROBE_AT(400);
-    if (wait_row) await_row(cx);
+    if (wait_row) await_row<GG>(cx);
     MGRIT_PROBE_AT(401);
 #pragma unroll
     for (int k = 0; k < NPT; ++k) {
         const Dec d = decompose_s(sv[k], n);
         double w[P + 1];
         lagrange_weights<P>(d.eps, w);
-        const double *src = cx.row + (d.e - SLW);
+        double tap[P + 1];
+        if constexpr (GG) {
+            // periodic taps straight from the (L2-resident) global row
+#pragma unroll
+            for (int c = 0; c <= P; ++c) {
+                int idx = d.e - SLW + c;
+                idx += idx < 0 ? n : 0;
+                idx -= idx >= n ? n : 0;
+                tap[c] = cx.zrow ? 0.0 : __ldcg(cx.grow + idx);
+            }
+        } else {
+            const double *src = cx.row + (d.e - SLW);
+#pragma unroll
+            for (int c = 0; c <= P; ++c) tap[c] = src[c];
+        }
         double acc = 0.0;
 #pragma unroll
         for (int c = 0; c <= P; ++c) {
-            const double prod = __dmul_rn(src[c], w[c]);
+            const double prod = __dmul_rn(tap[c], w[c]);
             acc = c == 0 ? prod : __dadd_rn(acc, prod);
         }
         v[k] = acc;
     }
     const int64_t set = L.shared ? 0 : t;
     const double *sig = L.sig_x + set * (int64_t)n + cx.base;
-    double sg[NPT];
+    // sigma in registers, or re-read (L1) for the widest rows
+    constexpr bool SGREG = NPT <= 8;
+    double sg[SGREG ? NPT : 1];
+    if constexpr (SGREG) {
 #pragma unroll
-    for (int k = 0; k < NPT; ++k) sg[k] = __ldg(sig + tid + k * NTC);
+        for (int k = 0; k < NPT; ++k) sg[k] = __ldg(sig + tid + k * NTC);
+    }
     // (I - diag(sig) D) x at local node li on slot buffer b
     auto imsd_at = [&](const double *b, int k, int li, double xi) -> double {
         double acc;
@@ -386,7 +431,10 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
             for (int q = 1; q <= RAD; ++q)
                 acc = __dadd_rn(acc, __dadd_rn(cmul<P>(RAD + q, b[li + q]), cmul<P>(RAD - q, b[li - q])));
         }
-        return __dsub_rn(xi, __dmul_rn(sg[k], acc));
+        double s_i;
+        if constexpr (SGREG) s_i = sg[k];
+        else s_i = __ldg(sig + li);
+        return __dsub_rn(xi, __dmul_rn(s_i, acc));
     };
     auto sumsq = [&]() -> double {
         double a = 0.0;
@@ -526,7 +574,7 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
                 const ArTok tk = ar_send<NPT, RAD, false, false>(cx, part, 0.0, v);
                 h[j] = ar_recv<false>(cx, tk).x;
 #pragma unroll
-                for (int k = 0; k < NPT; ++k) v[k] = fma(-h[j], bjr[k], v[k]);
+                for (int k = 0; k < NPT; ++k) v[k] = fma(-h[j], NPT <= 8 ? bjr[k] : bj[tid + k * NTC], v[k]);
             }
         }
         // norm of w (+ halo exchange of its edge values); the previous
@@ -621,7 +669,7 @@ __device__ __forceinline__ void cl_init(ClCtx &cx) {
 // --------------------------------------------------------- level phases --
 // Same phase semantics as phase_kernel (mgrit_b200.h MGRIT_PHASE_*), one
 // cluster per C-interval (persistent over intervals).
-template <int P, int NPT, bool LOWSYNC>
+template <int P, int NPT, bool LOWSYNC, bool GG>
 __global__ void __launch_bounds__(NTC) cl_phase_kernel(mgrit_level_desc L, mgrit_phase_args A, int32_t *status) {
     const int n = L.n_x;
     const int m = A.m;
@@ -662,8 +710,8 @@ __global__ void __launch_bounds__(NTC) cl_phase_kernel(mgrit_level_desc L, mgrit
         } else if (A.phase == MGRIT_PHASE_F_RES && c > 0) {
             store_chunk<NPT>(cx, U(t0), v);
         }
-        if (pub) publish_row(cx, pub);
-        else zero_row(cx);  // local, nothing to wait for
+        if (pub) publish_row<GG>(cx, pub);
+        else zero_row<GG>(cx);  // local, nothing to wait for
         bool have_pub = pub != nullptr;
 
         const bool last = (c + 1 == A.n_intervals);
@@ -679,13 +727,13 @@ __global__ void __launch_bounds__(NTC) cl_phase_kernel(mgrit_level_desc L, mgrit
 #pragma unroll 1
         for (int k = 1; k <= kmax; ++k) {
             const int64_t t = t0 + k;
-            cl_apply<P, NPT, false, LOWSYNC>(L, t - 1, cx, v, sv, have_pub);
+            cl_apply<P, NPT, false, LOWSYNC, GG>(L, t - 1, cx, v, sv, have_pub);
             have_pub = true;
             if (k < kmax) load_records_chunk<NPT>(cx, L, t, sv);
             if (k < m) {
                 add_forcing_chunk<NPT>(cx, v, Gr(t));
                 store_chunk<NPT>(cx, U(t), v);
-                if (k < kmax) publish_row(cx, U(t));
+                if (k < kmax) publish_row<GG>(cx, U(t));
                 continue;
             }
             if (A.phase == MGRIT_PHASE_FC) {
@@ -735,7 +783,7 @@ __global__ void __launch_bounds__(NTC) cl_phase_kernel(mgrit_level_desc L, mgrit
 }
 
 // ------------------------------------------------------ sequential sweep --
-template <int P, int NPT, bool NUMBA, bool LOWSYNC>
+template <int P, int NPT, bool NUMBA, bool LOWSYNC, bool GG>
 __global__ void __launch_bounds__(NTC) cl_sweep_kernel(mgrit_level_desc L, double *U, int64_t ldu, const double *G,
                                                        int64_t ldg, int zero_init, int32_t *gmres_iters,
                                                        int32_t *status) {
@@ -749,19 +797,19 @@ __global__ void __launch_bounds__(NTC) cl_sweep_kernel(mgrit_level_desc L, doubl
 #pragma unroll
         for (int k = 0; k < NPT; ++k) v[k] = 0.0;
         store_chunk<NPT>(cx, U, v);
-        zero_row(cx);
+        zero_row<GG>(cx);
     } else {
-        publish_row(cx, U);
+        publish_row<GG>(cx, U);
     }
 #pragma unroll 1
     for (int64_t t = 0; t < L.n_steps; ++t) {
-        const int cnt = cl_apply<P, NPT, NUMBA, LOWSYNC>(L, t, cx, v, sv, have_pub);
+        const int cnt = cl_apply<P, NPT, NUMBA, LOWSYNC, GG>(L, t, cx, v, sv, have_pub);
         have_pub = true;
         if (t + 1 < L.n_steps) load_records_chunk<NPT>(cx, L, t + 1, sv);
         add_forcing_chunk<NPT>(cx, v, G ? G + (t + 1) * ldg : nullptr);
         store_chunk<NPT>(cx, U + (t + 1) * ldu, v);
         if (gmres_iters && threadIdx.x == 0 && cx.rank == 0) gmres_iters[t] = cnt;
-        if (t + 1 < L.n_steps) publish_row(cx, U + (t + 1) * ldu);
+        if (t + 1 < L.n_steps) publish_row<GG>(cx, U + (t + 1) * ldu);
     }
     cluster_sync_all();
 }
@@ -774,7 +822,8 @@ inline bool cl_aligned(const void *p) { return ((uintptr_t)p & 15) == 0; }
 inline bool cl_eligible(const mgrit_level_desc *L) {
     if (L->kind != MGRIT_KIND_CORRECTED || L->dim != 1) return false;
     const int n = L->n_x;
-    if (n != 1024 && n != 2048 && n != 4096 && n != 8192) return false;
+    if (n != 1024 && n != 2048 && n != 4096 && n != 8192 && n != 16384) return false;
+    if (cl_gg(n) && L->gmres_lowsync) return false;  // register budget: MGS only at 16 nodes/thread
     if (L->gmres_max_iters < 1 || L->gmres_max_iters > kMaxKrylovCl) return false;
     if (cl_smem_bytes(n, L->gmres_max_iters) > (size_t)max_smem_optin()) return false;
     return true;
@@ -796,7 +845,8 @@ static int cl_dispatch_npt(int n, Fn &&f) {
         case 1024: return f(std::integral_constant<int, 1>{});
         case 2048: return f(std::integral_constant<int, 2>{});
         case 4096: return f(std::integral_constant<int, 4>{});
-        default: return f(std::integral_constant<int, 8>{});
+        case 8192: return f(std::integral_constant<int, 8>{});
+        default: return f(std::integral_constant<int, 16>{});
     }
 }
 
@@ -830,7 +880,8 @@ template <int P>
 int LaunchCl<P>::resident_clusters(const mgrit_level_desc *L) {
     const size_t smem = cl_smem_bytes(L->n_x, L->gmres_max_iters);
     return cl_dispatch_npt(L->n_x, [&](auto N) {
-        auto fn = cl_phase_kernel<P, decltype(N)::value, false>;
+        constexpr int NP = decltype(N)::value;
+        auto fn = cl_phase_kernel<P, NP, false, (NP > 8)>;
         if (cl_prep(fn, smem)) return 0;
         cudaLaunchAttribute attr[1];
         cudaLaunchConfig_t cfg = cl_config(fn, CS, smem, 0, attr);
@@ -862,8 +913,11 @@ int LaunchCl<P>::phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int
             }
             return (int)MGRIT_OK;
         };
-        if (L->gmres_lowsync) return launch(cl_phase_kernel<P, decltype(N)::value, true>);
-        return launch(cl_phase_kernel<P, decltype(N)::value, false>);
+        constexpr int NP = decltype(N)::value;
+        if constexpr (NP <= 8) {
+            if (L->gmres_lowsync) return launch(cl_phase_kernel<P, NP, true, false>);
+        }
+        return launch(cl_phase_kernel<P, NP, false, (NP > 8)>);
     });
     if (rc) return rc;
     return check_launch("level_phase(cluster)");
@@ -887,12 +941,16 @@ int LaunchCl<P>::sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const 
             }
             return (int)MGRIT_OK;
         };
-        if (L->gmres_lowsync) {
-            if (numba) return launch(cl_sweep_kernel<P, decltype(N)::value, true, true>);
-            return launch(cl_sweep_kernel<P, decltype(N)::value, false, true>);
+        constexpr int NP = decltype(N)::value;
+        constexpr bool GG = NP > 8;
+        if constexpr (NP <= 8) {
+            if (L->gmres_lowsync) {
+                if (numba) return launch(cl_sweep_kernel<P, NP, true, true, false>);
+                return launch(cl_sweep_kernel<P, NP, false, true, false>);
+            }
         }
-        if (numba) return launch(cl_sweep_kernel<P, decltype(N)::value, true, false>);
-        return launch(cl_sweep_kernel<P, decltype(N)::value, false, false>);
+        if (numba) return launch(cl_sweep_kernel<P, NP, true, false, GG>);
+        return launch(cl_sweep_kernel<P, NP, false, false, GG>);
     });
     if (rc) return rc;
     return check_launch("sequential_sweep(cluster)");

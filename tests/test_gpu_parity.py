@@ -619,3 +619,19 @@ def test_cluster_sweep_counts_match_oracle(P, cluster_policy):
     torch.cuda.synchronize()
     assert _rel(_np(Ud), Uo) < 1e-12
     assert list(_np(iters)) == log.counts
+
+
+def test_cluster_n16384_global_gather_matches_oracle(P, cluster_policy):
+    """n_x = 16384 (config 3's mesh): the cluster kernels gather the SL taps
+    straight from L2 (no shared-memory row copy) and publish rows with a
+    cluster barrier; full solve against the oracle."""
+    kw = dict(n_x=16384, n_t=128, wave_speed="C3", p=5, schedule=8, seed=2, max_iters=4, rtol=0.0)
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, olevels = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    rep, U = P.solve(cfg, levels)
+    orep, oU = O.solve(ocfg, olevels)
+    r0 = orep.residual_norms[0]
+    assert rep.iterations == orep.iterations
+    assert np.all(np.abs(rep.residual_norms - orep.residual_norms) <= 1e-12 * r0)
+    assert _rel(U, oU) <= U_TOL
