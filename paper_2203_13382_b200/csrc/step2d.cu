@@ -41,10 +41,24 @@ __device__ __forceinline__ double sl2d_at(const double *u, int nx, double sx, do
     double wx[P + 1], wy[P + 1];
     lagrange_weights<P>(dx.eps, wx);
     lagrange_weights<P>(dy.eps, wy);
+    constexpr int R = Stencil<P>::R;
+    double out = 0.0;
+    if (dx.e >= SL && dx.e + R < nx && dy.e >= SL && dy.e + R < nx) {
+        // interior window (almost every node): one base address, the taps
+        // are immediate offsets from it and one row stride
+        const double *r = u + (int64_t)(dy.e - SL) * nx + (dx.e - SL);
+#pragma unroll
+        for (int jy = 0; jy <= P; ++jy, r += nx) {
+            double acc = 0.0;
+#pragma unroll
+            for (int jx = 0; jx <= P; ++jx) acc = __dadd_rn(acc, __dmul_rn(wx[jx], __ldg(r + jx)));
+            out = __dadd_rn(out, __dmul_rn(wy[jy], acc));
+        }
+        return out;
+    }
     int cols[P + 1];
 #pragma unroll
     for (int j = 0; j <= P; ++j) cols[j] = wrapi(dx.e - SL + j, nx);
-    double out = 0.0;
 #pragma unroll
     for (int jy = 0; jy <= P; ++jy) {
         const double *r = u + (int64_t)wrapi(dy.e - SL + jy, nx) * nx;
@@ -64,6 +78,16 @@ __device__ __forceinline__ double imsd2d_at(const double *v, int nx, int ix, int
     const double *row = v + (int64_t)iy * nx;
     const double vi = row[ix];
     double dx = cmul<P>(RAD, vi), dy = cmul<P>(RAD, vi);
+    if (ix >= RAD && ix + RAD < nx && iy >= RAD && iy + RAD < nx) {
+        // interior: immediate offsets from the node's address
+        const double *c = row + ix;
+#pragma unroll
+        for (int q = 1; q <= RAD; ++q) {
+            dx = __dadd_rn(__dadd_rn(dx, cmul<P>(RAD + q, c[q])), cmul<P>(RAD - q, c[-q]));
+            dy = __dadd_rn(__dadd_rn(dy, cmul<P>(RAD + q, c[(int64_t)q * nx])), cmul<P>(RAD - q, c[-(int64_t)q * nx]));
+        }
+        return __dsub_rn(__dsub_rn(vi, __dmul_rn(sx, dx)), __dmul_rn(sy, dy));
+    }
 #pragma unroll
     for (int q = 1; q <= RAD; ++q) {
         dx = __dadd_rn(__dadd_rn(dx, cmul<P>(RAD + q, row[wrapi(ix + q, nx)])), cmul<P>(RAD - q, row[wrapi(ix - q, nx)]));
@@ -200,7 +224,7 @@ struct CoopSmem {
 };
 
 template <int P>
-__global__ void __launch_bounds__(kNT2) gmres2d_coop(Coop2D C) {
+__global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     cg::grid_group grid = cg::this_grid();
     __shared__ CoopSmem S;
     const mgrit_level_desc &L = C.L;
