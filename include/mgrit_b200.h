@@ -70,8 +70,10 @@ typedef struct mgrit_level_desc {
     double gmres_tol;       /* < 0 : fixed iteration count (tol None) */
     int32_t gmres_lowsync;  /* 0: classic MGS (the reference's loop, default);
                                1: low-synchronisation MGS -- same coefficients in
-                               exact arithmetic, one block reduction per Arnoldi
-                               step instead of k+1 (1D only) */
+                               exact arithmetic, one cluster all-reduce per
+                               Arnoldi step instead of k+1 (1D cluster kernels;
+                               the one-CTA kernels always run classic MGS, whose
+                               block reductions are cheaper there) */
     int32_t launch_policy;  /* MGRIT_LAUNCH_*: corrected 1D levels may run one
                                thread-block cluster (8 SMs) per row chain */
 } mgrit_level_desc;

@@ -823,7 +823,8 @@ inline bool cl_eligible(const mgrit_level_desc *L) {
     if (L->kind != MGRIT_KIND_CORRECTED || L->dim != 1) return false;
     const int n = L->n_x;
     if (n != 1024 && n != 2048 && n != 4096 && n != 8192 && n != 16384) return false;
-    if (cl_gg(n) && L->gmres_lowsync) return false;  // register budget: MGS only at 16 nodes/thread
+    // (n = 16384: 16 nodes per thread leave no registers for the low-sync
+    //  variant; those launches run classic MGS, see LaunchCl)
     if (L->gmres_max_iters < 1 || L->gmres_max_iters > kMaxKrylovCl) return false;
     if (cl_smem_bytes(n, L->gmres_max_iters) > (size_t)max_smem_optin()) return false;
     return true;

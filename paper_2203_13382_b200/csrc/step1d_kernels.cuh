@@ -46,11 +46,6 @@ struct GmresSmem {
     double H[(kMaxKrylov + 1) * kMaxKrylov];
     double cs[kMaxKrylov], sn[kMaxKrylov], g[kMaxKrylov + 1], y[kMaxKrylov];
     double red[2][33];
-    // low-synchronisation MGS (gmres_lowsync): Gram rows <b_j, b_i> (i < j),
-    // the projection coefficients, and per-warp partials of the fused dots
-    double gram[kMaxKrylov * kMaxKrylov];
-    double hv[kMaxKrylov];
-    double mred[2 * kMaxKrylov][32];
     int stop;
 };
 
@@ -201,7 +196,6 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
             // BLAS calls whose rounding is not reproducible anyway).
             const int K = L.gmres_max_iters;
             const double tol = L.gmres_tol;
-            const bool lowsync = L.gmres_lowsync != 0;
             GmresSmem &G = *cx.gs;
 
             // non-finite rhs -> NaN row + sticky flag (coarse_correction.py:181-182)
@@ -264,89 +258,6 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 // its entries arrive (rotation j needs h_j and h_{j+1} only), in
                 // the reference's order.
                 double hrun = 0.0;  // thread 0: column kk entry j after rotations < j
-                if (lowsync) {
-                    // Low-synchronisation MGS (Swirydowicz et al. 2020, MGS-ICWY
-                    // form): one pass forms d_j = <b_j, w> and the Gram row
-                    // <b_kk, b_j> for all j <= kk, one barrier publishes them,
-                    // and warp 0 recovers the MGS coefficients by the exact
-                    // identity h_j = d_j - sum_{i<j} <b_j, b_i> h_i, so the
-                    // kk+1 dependent reductions of MGS become one.
-                    constexpr int NW = NT / 32;
-                    const int lane = tid & 31, warp = tid >> 5;
-                    if (kk == 5) MGRIT_PROBE_AT(301);
-#pragma unroll 1
-                    for (int jb = 0; jb <= kk; jb += 4) {
-                        const double *bp[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int j = jb + q;
-                            bp[q] = j < kk ? cx.bvec(j, n) : cx.rowbuf;
-                        }
-                        double pd[4] = {0.0, 0.0, 0.0, 0.0}, pg[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                        for (int k = 0; k < NPT; ++k) {
-                            const int i = tid + k * NT;
-                            if (F || i < n) {
-                                const double bk = cx.rowbuf[i];
-#pragma unroll
-                                for (int q = 0; q < 4; ++q) {
-                                    const double b = bp[q][i];
-                                    pd[q] = fma(b, v[k], pd[q]);
-                                    pg[q] = fma(b, bk, pg[q]);
-                                }
-                            }
-                        }
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const double sd = warp_sum(pd[q]), sg2 = warp_sum(pg[q]);
-                            if (lane == 0 && jb + q <= kk) {
-                                G.mred[jb + q][warp] = sd;
-                                G.mred[kMaxKrylov + jb + q][warp] = sg2;
-                            }
-                        }
-                    }
-                    if (kk == 5) MGRIT_PROBE_AT(302);
-                    __syncthreads();
-                    if (kk == 5) MGRIT_PROBE_AT(303);
-                    if (warp == 0) {
-                        // lane q < kk+1: d_q; lane kk+1+i: Gram entry <b_kk, b_i>, i < kk
-                        double val = 0.0;
-                        if (lane <= kk) val = tree_sum<NW>(G.mred[lane]);
-                        else if (lane <= 2 * kk) val = tree_sum<NW>(G.mred[kMaxKrylov + lane - kk - 1]);
-                        if (lane <= kk) G.hv[lane] = val;
-                        else if (lane <= 2 * kk) G.gram[kk * kMaxKrylov + lane - kk - 1] = val;
-                        __syncwarp();
-                        if (lane == 0) {
-                            for (int j = 0; j <= kk; ++j) {
-                                double h = G.hv[j];
-                                for (int i = 0; i < j; ++i) h = fma(-G.gram[j * kMaxKrylov + i], G.hv[i], h);
-                                G.hv[j] = h;
-                                if (j == 0) {
-                                    hrun = h;
-                                } else {
-                                    const double c = G.cs[j - 1], sn = G.sn[j - 1];
-                                    const double tmp = __dadd_rn(__dmul_rn(c, hrun), __dmul_rn(sn, h));
-                                    hrun = __dadd_rn(__dmul_rn(-sn, hrun), __dmul_rn(c, h));
-                                    G.H[(j - 1) * kMaxKrylov + kk] = tmp;
-                                }
-                            }
-                        }
-                    }
-                    if (kk == 5) MGRIT_PROBE_AT(304);
-                    __syncthreads();
-                    if (kk == 5) MGRIT_PROBE_AT(305);
-#pragma unroll 1
-                    for (int j = 0; j <= kk; ++j) {
-                        const double hj = G.hv[j];
-                        const double *bp = j == kk ? cx.rowbuf : cx.bvec(j, n);
-#pragma unroll
-                        for (int k = 0; k < NPT; ++k) {
-                            const int i = tid + k * NT;
-                            if (F || i < n) v[k] = fma(-hj, bp[i], v[k]);
-                        }
-                    }
-                    if (kk == 5) MGRIT_PROBE_AT(306);
-                } else {
                 double bc[NPT];
                 {
                     const double *b0p = kk == 0 ? cx.rowbuf : cx.bvec(0, n);
@@ -398,7 +309,6 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 for (int j = 0; j <= kk; j += 2) {
                     mgs_step(j, bc, bo);
                     if (j + 1 <= kk) mgs_step(j + 1, bo, bc);
-                }
                 }
                 MGRIT_PROBE_AT(12 + 8 * kk);
                 const double nrm = sqrt(block_sum2<NT>(sumsq4(), cx));
@@ -552,7 +462,7 @@ __device__ __forceinline__ RowCtx make_ctx(double *sm, int n, int nbs, double *s
 // apply_rows: one CTA per row (persistent over rows)
 
 template <int P, int KIND, int NT, int NPT, bool F>
-__global__ void __launch_bounds__(NT) rows_kernel(mgrit_level_desc L, RowsArgs a, int nbs, double *scratch,
+__global__ void __launch_bounds__(NT, 1) rows_kernel(mgrit_level_desc L, RowsArgs a, int nbs, double *scratch,
                                                   int32_t *status) {
     extern __shared__ double sm[];
     const int n = L.n_x;
@@ -587,7 +497,7 @@ __global__ void __launch_bounds__(NT) rows_kernel(mgrit_level_desc L, RowsArgs a
 // fused level phases: one CTA per C-interval (persistent over intervals)
 
 template <int P, int KIND, int NT, int NPT, bool F>
-__global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_phase_args A, int nbs,
+__global__ void __launch_bounds__(NT, 1) phase_kernel(mgrit_level_desc L, mgrit_phase_args A, int nbs,
                                                    double *scratch, int32_t *status) {
     extern __shared__ double sm[];
     // The next step's departure records are prefetched into registers while
@@ -741,7 +651,7 @@ __global__ void __launch_bounds__(NT) phase_kernel(mgrit_level_desc L, mgrit_pha
 // sequential sweep: one CTA steps the whole level
 
 template <int P, int KIND, int NT, int NPT, bool F, bool NUMBA>
-__global__ void __launch_bounds__(NT) sweep_kernel(mgrit_level_desc L, double *U, int64_t ldu,
+__global__ void __launch_bounds__(NT, 1) sweep_kernel(mgrit_level_desc L, double *U, int64_t ldu,
                                                    const double *G, int64_t ldg, int zero_init,
                                                    int32_t *gmres_iters, int nbs, double *scratch,
                                                    int32_t *status) {

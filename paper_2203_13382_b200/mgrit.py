@@ -60,7 +60,8 @@ class GmresConfig:
     tol: float | None = None
     # "mgs": the reference's modified Gram-Schmidt loop; "mgs_lowsync": the
     # same projection coefficients via one fused reduction per Arnoldi step
-    # (Gram-corrected, 1D levels only) -- equal in exact arithmetic, not bitwise
+    # (Gram-corrected) on the 1D cluster kernels, where every reduction is a
+    # DSMEM round trip -- equal in exact arithmetic, not bitwise
     variant: str = "mgs"
 
     def __post_init__(self):
