@@ -82,12 +82,21 @@ def _dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region.
+
+    Every sample line is stamped with the host clock, so the summary can keep
+    only the samples taken between mark("start") and mark("stop").  A timed
+    region shorter than a few sampling periods (cfg1: ~4 ms) falls back to the
+    samples of the surrounding load (warm-up + an untimed tail of the same
+    solves) and says so in "window"."""
+
+    PERIOD_MS = 20
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.marks: dict[str, float] = {}
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -95,17 +104,27 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.perf_counter() + 5.0          # wait until nvidia-smi is live
+            while not self.lines and time.perf_counter() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, name: str):
+        self.marks[name] = time.perf_counter()
+
+    def n_in(self, a: str, b: str) -> int:
+        ta, tb = self.marks.get(a, 0.0), self.marks.get(b, float("inf"))
+        return sum(1 for t, _ in self.lines if ta <= t <= tb)
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -115,10 +134,15 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, min_samples: int = 3):
+        window = "timed"
+        sel = [ln for t, ln in self.lines if self.marks.get("start", 0) <= t <= self.marks.get("stop", 1e300)]
+        if len(sel) < min_samples:
+            window = "load (warm-up + timed + untimed tail of the same solves; timed region too short)"
+            sel = [ln for t, ln in self.lines if self.marks.get("load", 0) <= t <= self.marks.get("end", 1e300)]
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in sel:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -131,7 +155,8 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window,
+                "period_ms": self.PERIOD_MS}
 
 
 # ---------------------------------------------------------------------------
@@ -200,22 +225,34 @@ def run_gpu(args):
         return T.solve_time_parallel(cfg, levels, comm, iterate0=iterate0, out=out)[0]
 
     # warm-up (also compiles CUDA graphs / sets kernel attributes)
-    for _ in range(args.warmup):
-        rep = do_solve()
+    rep = do_solve()
     barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        clk.mark("load")
+        for _ in range(args.warmup - 1):
+            rep = do_solve()
         barrier()
+        clk.mark("start")
         start.record()
         for _ in range(args.steps):
             rep = do_solve()
         stop.record()
         barrier()
-    ms = start.elapsed_time(stop) / args.steps
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        clk.mark("stop")
+        ms = start.elapsed_time(stop) / args.steps
+        if dist is not None:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        # untimed tail of the same solves so a very short timed region still
+        # has clock samples taken under this load (reported as such); the
+        # count derives from the all-reduced time, so every rank agrees
+        if ms * args.steps < 3 * ClockSampler.PERIOD_MS + 60:
+            for _ in range(min(int(300.0 / max(ms, 1e-3)) + 1, 2000)):
+                do_solve()
+            barrier()
+        clk.mark("end")
     # the time-sharded solve does the whole problem once across all ranks
     # (strong scaling); replicas are not used
     value = n_dof / (ms / 1e3)
