@@ -199,7 +199,10 @@ def run_gpu(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # eager communicator setup: every rank takes part in the first
+        # collective (the engine's first op may be a one-sided P2P batch)
+        dist.barrier()
     kw = dict(CONFIGS[args.config], gmres_variant=args.gmres_variant)
     P.set_launch_policy(args.launch_policy)
     cfg = P.SolverConfig(**kw)

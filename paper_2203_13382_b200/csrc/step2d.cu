@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -269,14 +270,31 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             }
         }
     };
-    auto reduce_nodes = [&](auto &&val) {
+    // for_nodes fused with the per-warp-block reduction of body's return
+    // value: same node -> (lane, k) mapping and the same per-lane order as
+    // reduce_nodes, so the partials are bit-identical to the two-pass form
+    // while the vectors are read once
+    auto for_nodes_red = [&](auto &&body) {
         double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
         for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
+            const int64_t base = wb * kWB;
+            const int iy0 = row_blocks ? (int)(base / nx) : 0;
+            const int ix0 = row_blocks ? (int)(base - (int64_t)iy0 * nx) : 0;
             double acc = 0.0;
 #pragma unroll
             for (int k = 0; k < kWBPerLane; ++k) {
-                const int64_t i = wb * kWB + lane + 32 * k;
-                if (i < n) acc = __dadd_rn(acc, val(i));
+                const int64_t i = base + lane + 32 * k;
+                if (i < n) {
+                    int ix, iy;
+                    if (row_blocks) {
+                        ix = ix0 + lane + 32 * k;
+                        iy = iy0;
+                    } else {
+                        iy = (int)((unsigned)i / (unsigned)nx);
+                        ix = (int)i - iy * nx;
+                    }
+                    acc = __dadd_rn(acc, body(i, ix, iy));
+                }
             }
             acc = warp_sum(acc);
             if (lane == 0 && active_cta) pb[wb] = acc;
@@ -311,12 +329,12 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
         int bad = 0;
         if (active) {
             const double *u = a.U_in + b * a.ld_in;
-            for_nodes([&](int64_t i, int ix, int iy) {
+            for_nodes_red([&](int64_t i, int ix, int iy) {
                 const double v = sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
                 w[i] = v;
                 if (!isfinite(v)) bad = 1;
+                return __dmul_rn(v, v);
             });
-            reduce_nodes([&](int64_t i) { return __dmul_rn(w[i], w[i]); });
         }
         bad = __syncthreads_or(bad);
         if (active && tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
@@ -347,10 +365,11 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             const double *bk = basis + (int64_t)kk * n;
             // w = A b_kk ; inner product with b_0
             if (run) {
-                for_nodes([&](int64_t i, int ix, int iy) {
-                    w[i] = imsd2d_at<P>(bk, nx, ix, iy, __ldg(gx + i), __ldg(gy + i));
+                for_nodes_red([&](int64_t i, int ix, int iy) {
+                    const double x = imsd2d_at<P>(bk, nx, ix, iy, __ldg(gx + i), __ldg(gy + i));
+                    w[i] = x;
+                    return __dmul_rn(basis[i], x);
                 });
-                reduce_nodes([&](int64_t i) { return __dmul_rn(basis[i], w[i]); });
             }
             double hrun = 0.0;
             for (int j = 0; j <= kk; ++j) {
@@ -369,8 +388,19 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                 if (run) {
                     const double *bj = basis + (int64_t)j * n;
                     const double *bn = j < kk ? basis + (int64_t)(j + 1) * n : nullptr;
-                    for_nodes([&](int64_t i, int ix, int iy) { w[i] = fma(-h, bj[i], w[i]); });
-                    reduce_nodes([&](int64_t i) { return __dmul_rn(bn ? bn[i] : w[i], w[i]); });
+                    if (bn) {
+                        for_nodes_red([&](int64_t i, int ix, int iy) {
+                            const double x = fma(-h, bj[i], w[i]);
+                            w[i] = x;
+                            return __dmul_rn(bn[i], x);
+                        });
+                    } else {
+                        for_nodes_red([&](int64_t i, int ix, int iy) {
+                            const double x = fma(-h, bj[i], w[i]);
+                            w[i] = x;
+                            return __dmul_rn(x, x);
+                        });
+                    }
                 }
             }
             const double nrm = sqrt(gtotal());
@@ -412,7 +442,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
         }
         __syncthreads();
         if (active) {
-            for_nodes([&](int64_t i, int ix, int iy) {
+            for_nodes_red([&](int64_t i, int ix, int iy) {
                 double x = 0.0;
                 if (anybad) {
                     x = __longlong_as_double(0x7ff8000000000000LL);
@@ -421,10 +451,9 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                 }
                 const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
                 x = a.U_sub ? __dsub_rn(__dadd_rn(g, x), a.U_sub[b * a.ld_sub + i]) : __dadd_rn(x, g);
-                w[i] = x;
                 if (a.out) a.out[b * a.ld_out + i] = x;
+                return __dmul_rn(x, x);
             });
-            reduce_nodes([&](int64_t i) { return __dmul_rn(w[i], w[i]); });
         }
         const double tot = gtotal();
         if (active && tid == 0 && chunk == 0) {
@@ -462,6 +491,18 @@ int64_t capacity2d(const mgrit_level_desc *L) {
         constexpr int P = decltype(PP)::value;
         return coop_capacity((const void *)gmres2d_coop<P>);
     });
+}
+
+// systems solved concurrently by the cooperative kernel.  0 = as many as
+// the resident grid allows; MGRIT_COOP_ROWS overrides (tuning experiments)
+static int64_t coop_rows_cap(const mgrit_level_desc *L) {
+    (void)L;
+    static int64_t env = -1;
+    if (env < 0) {
+        const char *e = getenv("MGRIT_COOP_ROWS");
+        env = e ? atoll(e) : 0;
+    }
+    return env;
 }
 
 static int64_t coop_row_bytes(const mgrit_level_desc *L) {
@@ -506,6 +547,8 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             const void *fn = (const void *)gmres2d_coop<P>;
             const int G = coop_capacity(fn);
             int64_t rows = r.B < G ? r.B : G;
+            const int64_t cap = coop_rows_cap(L);
+            if (cap > 0 && rows > cap) rows = cap;
             const int64_t per_row = coop_row_bytes(L);
             if (scratch_bytes - 4096 < per_row) return (int)MGRIT_EINVAL;
             if (rows > (scratch_bytes - 4096) / per_row) rows = (scratch_bytes - 4096) / per_row;
