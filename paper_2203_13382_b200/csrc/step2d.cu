@@ -8,11 +8,13 @@
 //  * forward Euler: SL into scratch, then the explicit correction pass;
 //  * corrected (SL + MGS-GMRES on I - diag(sx) Dx - diag(sy) Dy): one
 //    cooperative kernel over the batch; each system is split into chunks
-//    over the resident CTAs and every MGS inner product is a grid-wide,
-//    fixed-order reduction (per-chunk partials, grid.sync, ordered sum).
+//    over the resident CTAs and every MGS inner product is a system-wide,
+//    fixed-order reduction (per-warp-block partials, a barrier over the
+//    system's CTAs only, ordered sum); systems never wait for each other.
 // The fused MGRIT phases are composed on the host from these batched launches
 // with strided row pointers (same semantics as the 1D phase_kernel).
 #include <cooperative_groups.h>
+#include <cuda/atomic>
 
 #include <cstdio>
 #include <cstdlib>
@@ -213,7 +215,7 @@ struct Coop2D {
     double *w;                // [rows_per_round][n]
     double *part;             // [2][rows_per_round][nwb] reduction partials
     int *flags;               // [rows_per_round][chunks] non-finite rhs
-    int *stopflags;           // [rows_per_round]
+    unsigned int *bar;        // [rows_per_round] per-system barrier counters (zeroed per launch)
     int32_t *gmres_iters;
     int32_t *status;
 };
@@ -226,7 +228,6 @@ struct CoopSmem {
 
 template <int P>
 __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ CoopSmem S;
     const mgrit_level_desc &L = C.L;
     const Rows2D &a = C.a;
@@ -300,34 +301,46 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             if (lane == 0 && active_cta) pb[wb] = acc;
         }
     };
-    // grid barrier, then the fixed-order total of the system's partials
-    auto gtotal = [&]() -> double {
-        grid.sync();
-        double tot = 0.0;
-        if (active_cta) {
-            const double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
-            double acc = 0.0;
-            for (int64_t q = tid; q < nwb; q += kNT2) acc = __dadd_rn(acc, pb[q]);
-            tot = block_sum<kNT2>(acc, S.red);
-        } else {
-            __syncthreads();
+    // Barrier over the `chunks` CTAs of this system slot only (all CTAs are
+    // co-resident: cooperative launch).  Monotonic per-slot counter, release
+    // on arrival, acquire on the spin (which also invalidates stale L1
+    // lines), so slots never wait for each other: a system that converges
+    // early frees HBM bandwidth for the rest instead of idling in lock-step.
+    unsigned int gen = 0;
+    auto ssync = [&]() {
+        __syncthreads();
+        if (tid == 0) {
+            ++gen;
+            cuda::atomic_ref<unsigned int, cuda::thread_scope_device> ctr(C.bar[slot]);
+            ctr.fetch_add(1u, cuda::memory_order_release);
+            const unsigned int target = gen * (unsigned int)C.chunks;
+            while (ctr.load(cuda::memory_order_acquire) < target) {
+            }
         }
+        __syncthreads();
+    };
+    // system barrier, then the fixed-order total of the system's partials
+    auto gtotal = [&]() -> double {
+        ssync();
+        const double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
+        double acc = 0.0;
+        for (int64_t q = tid; q < nwb; q += kNT2) acc = __dadd_rn(acc, pb[q]);
+        const double tot = block_sum<kNT2>(acc, S.red);
         pbuf ^= 1;
         return tot;
     };
+    if (!active_cta) return;
 
-    for (int64_t round0 = 0; round0 < a.B; round0 += C.rows_per_round) {
-        const int64_t b = round0 + slot;
-        const bool active = active_cta && b < a.B;
-        const int64_t t = active ? row_t(a, b) : 0;
+    double *basis = C.basis + (int64_t)slot * (K + 1) * n;
+    double *w = C.w + (int64_t)slot * n;
+    for (int64_t b = slot; b < a.B; b += C.rows_per_round) {
+        const int64_t t = row_t(a, b);
         const int64_t set = L.shared ? 0 : t;
         const double *sx = L.s_x + set * n, *sy = L.s_y + set * n;
         const double *gx = L.sig_x + set * n, *gy = L.sig_y + set * n;
-        double *basis = C.basis + (int64_t)slot * (K + 1) * n;
-        double *w = C.w + (int64_t)slot * n;
         // ---- SL rhs into w, non-finite flag, beta
         int bad = 0;
-        if (active) {
+        {
             const double *u = a.U_in + b * a.ld_in;
             for_nodes_red([&](int64_t i, int ix, int iy) {
                 const double v = sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
@@ -337,44 +350,38 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             });
         }
         bad = __syncthreads_or(bad);
-        if (active && tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
+        if (tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
         const double beta = sqrt(gtotal());
         int anybad = 0;
-        if (active && tid == 0)
+        if (tid == 0)
             for (int k = 0; k < C.chunks; ++k) anybad |= C.flags[(int64_t)slot * C.chunks + k];
         anybad = __syncthreads_or(anybad);
         int done = 0;
-        const bool skip = !active || anybad || beta == 0.0;
-        if (active && anybad && tid == 0 && chunk == 0) atomicExch(C.status, 1);
+        const bool skip = anybad || beta == 0.0;
+        if (anybad && tid == 0 && chunk == 0) atomicExch(C.status, 1);
         if (!skip) {
             const double yb = 1.0 / beta;
             for_nodes([&](int64_t i, int ix, int iy) { basis[i] = div_rcp(w[i], beta, yb); });
         }
         if (tid == 0) S.stop = skip ? 1 : 0;
-        if (active_cta && tid == 0 && chunk == 0) C.stopflags[slot] = skip ? 1 : 0;
         double g_k = beta;
-        // grid-uniform iteration loop; it ends when every system has stopped
+        // the stop test is evaluated from the same totals in every CTA of the
+        // system, so all of them leave the loop at the same kk
         for (int kk = 0; kk < K; ++kk) {
             __syncthreads();
-            const bool run = !S.stop;
-            grid.sync();  // b_kk and the stop flags visible everywhere
-            int live = 0;
-            for (int q = tid; q < C.rows_per_round; q += kNT2)
-                if (round0 + q < a.B && !C.stopflags[q]) live = 1;
-            if (!__syncthreads_or(live)) break;
+            if (S.stop) break;
+            ssync();  // b_kk complete in every chunk (the stencil reads across chunks)
             const double *bk = basis + (int64_t)kk * n;
             // w = A b_kk ; inner product with b_0
-            if (run) {
-                for_nodes_red([&](int64_t i, int ix, int iy) {
-                    const double x = imsd2d_at<P>(bk, nx, ix, iy, __ldg(gx + i), __ldg(gy + i));
-                    w[i] = x;
-                    return __dmul_rn(basis[i], x);
-                });
-            }
+            for_nodes_red([&](int64_t i, int ix, int iy) {
+                const double x = imsd2d_at<P>(bk, nx, ix, iy, __ldg(gx + i), __ldg(gy + i));
+                w[i] = x;
+                return __dmul_rn(basis[i], x);
+            });
             double hrun = 0.0;
             for (int j = 0; j <= kk; ++j) {
                 const double h = gtotal();
-                if (run && tid == 0) {
+                if (tid == 0) {
                     if (j == 0) {
                         hrun = h;
                     } else {
@@ -385,48 +392,42 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                     }
                 }
                 // w -= h b_j, fused with the next inner product (b_{j+1} or ||w||^2)
-                if (run) {
-                    const double *bj = basis + (int64_t)j * n;
-                    const double *bn = j < kk ? basis + (int64_t)(j + 1) * n : nullptr;
-                    if (bn) {
-                        for_nodes_red([&](int64_t i, int ix, int iy) {
-                            const double x = fma(-h, bj[i], w[i]);
-                            w[i] = x;
-                            return __dmul_rn(bn[i], x);
-                        });
-                    } else {
-                        for_nodes_red([&](int64_t i, int ix, int iy) {
-                            const double x = fma(-h, bj[i], w[i]);
-                            w[i] = x;
-                            return __dmul_rn(x, x);
-                        });
-                    }
+                const double *bj = basis + (int64_t)j * n;
+                const double *bn = j < kk ? basis + (int64_t)(j + 1) * n : nullptr;
+                if (bn) {
+                    for_nodes_red([&](int64_t i, int ix, int iy) {
+                        const double x = fma(-h, bj[i], w[i]);
+                        w[i] = x;
+                        return __dmul_rn(bn[i], x);
+                    });
+                } else {
+                    for_nodes_red([&](int64_t i, int ix, int iy) {
+                        const double x = fma(-h, bj[i], w[i]);
+                        w[i] = x;
+                        return __dmul_rn(x, x);
+                    });
                 }
             }
             const double nrm = sqrt(gtotal());
-            if (run) {
-                const bool brk = nrm <= __dmul_rn(1e-14, beta);
-                if (!brk) {
-                    const double yn = 1.0 / nrm;
-                    double *bn = basis + (int64_t)(kk + 1) * n;
-                    for_nodes([&](int64_t i, int ix, int iy) { bn[i] = div_rcp(w[i], nrm, yn); });
-                }
-                __syncthreads();
-                if (tid == 0) {
-                    const double den = hypot(hrun, nrm);
-                    const double c = __ddiv_rn(hrun, den), sn = __ddiv_rn(nrm, den);
-                    S.cs[kk] = c;
-                    S.sn[kk] = sn;
-                    S.H[kk * kMaxK2 + kk] = den;
-                    const double gn = __dmul_rn(-sn, g_k);
-                    S.g[kk] = __dmul_rn(c, g_k);
-                    S.g[kk + 1] = gn;
-                    g_k = gn;
-                    S.stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta)) || kk + 1 == K;
-                    if (chunk == 0 && S.stop) C.stopflags[slot] = 1;
-                }
-                done = kk + 1;
+            const bool brk = nrm <= __dmul_rn(1e-14, beta);
+            if (!brk) {
+                const double yn = 1.0 / nrm;
+                double *bn = basis + (int64_t)(kk + 1) * n;
+                for_nodes([&](int64_t i, int ix, int iy) { bn[i] = div_rcp(w[i], nrm, yn); });
             }
+            if (tid == 0) {
+                const double den = hypot(hrun, nrm);
+                const double c = __ddiv_rn(hrun, den), sn = __ddiv_rn(nrm, den);
+                S.cs[kk] = c;
+                S.sn[kk] = sn;
+                S.H[kk * kMaxK2 + kk] = den;
+                const double gn = __dmul_rn(-sn, g_k);
+                S.g[kk] = __dmul_rn(c, g_k);
+                S.g[kk + 1] = gn;
+                g_k = gn;
+                S.stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta));
+            }
+            done = kk + 1;
         }
         __syncthreads();
         // back substitution (warp 0, column-oriented), x = sum_j b_j y_j, output form
@@ -441,26 +442,24 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             }
         }
         __syncthreads();
-        if (active) {
-            for_nodes_red([&](int64_t i, int ix, int iy) {
-                double x = 0.0;
-                if (anybad) {
-                    x = __longlong_as_double(0x7ff8000000000000LL);
-                } else if (!skip) {
-                    for (int j = 0; j < done; ++j) x = fma(basis[(int64_t)j * n + i], S.y[j], x);
-                }
-                const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
-                x = a.U_sub ? __dsub_rn(__dadd_rn(g, x), a.U_sub[b * a.ld_sub + i]) : __dadd_rn(x, g);
-                if (a.out) a.out[b * a.ld_out + i] = x;
-                return __dmul_rn(x, x);
-            });
-        }
+        for_nodes_red([&](int64_t i, int ix, int iy) {
+            double x = 0.0;
+            if (anybad) {
+                x = __longlong_as_double(0x7ff8000000000000LL);
+            } else if (!skip) {
+                for (int j = 0; j < done; ++j) x = fma(basis[(int64_t)j * n + i], S.y[j], x);
+            }
+            const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
+            x = a.U_sub ? __dsub_rn(__dadd_rn(g, x), a.U_sub[b * a.ld_sub + i]) : __dadd_rn(x, g);
+            if (a.out) a.out[b * a.ld_out + i] = x;
+            return __dmul_rn(x, x);
+        });
         const double tot = gtotal();
-        if (active && tid == 0 && chunk == 0) {
+        if (tid == 0 && chunk == 0) {
             if (a.partial) a.partial[b] = tot;    // per-row sum of squares
             if (C.gmres_iters) C.gmres_iters[b] = anybad ? -1 : done;
         }
-        grid.sync();
+        ssync();  // every chunk is done with this slot's buffers
     }
 }
 
@@ -493,21 +492,31 @@ int64_t capacity2d(const mgrit_level_desc *L) {
     });
 }
 
-// systems solved concurrently by the cooperative kernel.  0 = as many as
-// the resident grid allows; MGRIT_COOP_ROWS overrides (tuning experiments)
+// Systems solved concurrently by the cooperative kernel: as many as keep
+// their working Krylov vectors (~6 of n fp64 each at the tolerance-mode
+// iteration counts) inside ~80% of L2, so the MGS passes stream from L2
+// rather than HBM (measured on B200: cfg4 64 -> 8 systems 679 -> 618 ms,
+// cfg5 32 -> 2 systems 4381 -> 3988 ms per solve).  MGRIT_COOP_ROWS
+// overrides (0 = as many as the resident grid allows).
 static int64_t coop_rows_cap(const mgrit_level_desc *L) {
-    (void)L;
-    static int64_t env = -1;
-    if (env < 0) {
+    static int64_t env = -2;
+    if (env == -2) {
         const char *e = getenv("MGRIT_COOP_ROWS");
-        env = e ? atoll(e) : 0;
+        env = e ? atoll(e) : -1;
     }
-    return env;
+    if (env >= 0) return env;
+    int dev = 0, l2 = 126 << 20;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    const int vecs = L->gmres_max_iters + 2 < 6 ? L->gmres_max_iters + 2 : 6;
+    const int64_t per = (int64_t)vecs * L->n_points * 8;
+    const int64_t r = (int64_t)(0.8 * (double)l2) / (per > 0 ? per : 1);
+    return r < 1 ? 1 : r;
 }
 
 static int64_t coop_row_bytes(const mgrit_level_desc *L) {
     const int64_t n = L->n_points, nwb = (n + kWB - 1) / kWB;
-    return 8 * ((int64_t)(L->gmres_max_iters + 2) * n + 2 * nwb) + 4 * 4096 + 4;
+    return 8 * ((int64_t)(L->gmres_max_iters + 2) * n + 2 * nwb) + 4 * 4096 + 8;
 }
 
 int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows) {
@@ -567,7 +576,11 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             C.w = C.basis + rows * (int64_t)(L->gmres_max_iters + 1) * n;
             C.part = C.w + rows * n;
             C.flags = (int *)(C.part + 2 * rows * nwb);
-            C.stopflags = C.flags + rows * chunks;
+            C.bar = (unsigned int *)(C.flags + rows * chunks);
+            if (cudaMemsetAsync(C.bar, 0, rows * sizeof(unsigned int), st) != cudaSuccess) {
+                set_error("cudaMemsetAsync", cudaGetLastError());
+                return (int)MGRIT_ECUDA;
+            }
             C.gmres_iters = r.gmres_iters;
             C.status = status;
             void *args[] = {&C};
