@@ -448,6 +448,34 @@ def test_sl_step_batch_2d_bitwise(P, p, speed):
 
 
 @pytest.mark.parametrize("p", [1, 3, 5])
+@pytest.mark.parametrize("speed,cfl", [("B4", 0.85), ("C5", 0.85), ("B4", 100.0)])
+def test_sl_step_batch_2d_large_mesh_bitwise(P, p, speed, cfl):
+    """A 256^2 mesh (interior fast path on most nodes, wrapped windows at the
+    edges), including dt = 100h whose departures wrap around the domain:
+    step_batch / f_relax / residual bit-identical to the reference."""
+    nx = 256
+    kw = dict(n_x=nx, n_t=8, dim=2, wave_speed=speed, p=p, schedule=4, dt=cfl * 2.0 / nx)
+    cfg, ocfg = _cfg_pair(P, kw)
+    coords, olevels = _fine_coords(ocfg)
+    levels = P.build_hierarchy(cfg, fine_coords=coords)
+    rng = np.random.default_rng(29)
+    npts = nx * nx
+    U = rng.standard_normal((8, npts))
+    t = np.arange(8)
+    got = _np(levels[0].step_batch(t, torch.from_numpy(U).to(dev())))
+    assert np.array_equal(got, olevels[0].step_batch(t, U))
+    G = rng.standard_normal((9, npts))
+    U0 = rng.standard_normal((9, npts))
+    Ud = torch.from_numpy(U0.copy()).to(dev())
+    Uo = U0.copy()
+    P.f_relax(levels[0], Ud, torch.from_numpy(G).to(dev()))
+    O.f_relax(olevels[0], Uo, G)
+    assert np.array_equal(_np(Ud), Uo)
+    Rd = P.residual(levels[0], torch.from_numpy(U0).to(dev()), torch.from_numpy(G).to(dev()))
+    assert np.array_equal(_np(Rd), O.residual(olevels[0], U0, G))
+
+
+@pytest.mark.parametrize("p", [1, 3, 5])
 @pytest.mark.parametrize("mode", ["fixed", "tolerance"])
 def test_corrected_step_2d_matches_oracle(P, p, mode):
     """2D corrected operator (cooperative grid-wide MGS-GMRES): rows within
