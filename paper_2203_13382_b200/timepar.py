@@ -16,9 +16,21 @@ The only data that moves per sharded level and V-cycle:
 One state row each (8 n bytes), NCCL send/recv over NVLink.  The
 convergence norm all-gathers the per-interval partial sums and every rank
 adds them in global interval order, so histories are bitwise independent
-of P.  Levels whose interval count is not divisible by P, and always the
-coarsest level, are replicated: their forcing is all-gathered and every
-rank runs the remaining hierarchy redundantly (no further communication).
+of P.
+
+A coarse level whose interval count I does not divide by P is split over
+Q = gcd(I, Q_finer) rank GROUPS instead of being replicated: the P ranks
+form Q groups of P/Q consecutive ranks, every rank of group w owns
+intervals [w I/Q, (w+1) I/Q) (the group's members compute them
+redundantly), and the row exchanges go between counterpart ranks of
+neighbouring groups (rank r <-> r +- P/Q).  Since Q divides the finer
+level's group count, a rank's finer C-indices always lie inside its
+group's coarse range, so injection stays rank-local; the restriction is
+all-gathered once per V-cycle (one C-residual slab per group).  Only the
+coarsest level (Q = 1) is fully replicated.  This matters where coarse
+levels are bandwidth-bound batched solves (2D, config 5: level 2 has 4
+intervals, so at P = 8 each group of 2 ranks solves 1 of them instead of
+every rank solving all 4).
 
 The engine is written against a small backend interface (``phase``,
 ``sweep``, ``total``) so the same sharding / exchange logic runs on the
@@ -29,6 +41,7 @@ a numpy restatement of the phase semantics over gloo.
 from __future__ import annotations
 
 import ctypes
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -60,12 +73,13 @@ class Comm:
     def _global(self, r):
         return dist.get_global_rank(self.group, r) if self.group is not None else r
 
-    def shift(self, send: torch.Tensor | None, recv: torch.Tensor | None, direction: int):
-        """direction=+1: rank r sends to r+1 and receives from r-1; -1 reverses."""
+    def shift(self, send: torch.Tensor | None, recv: torch.Tensor | None, direction: int, stride: int = 1):
+        """direction=+1: rank r sends to r+stride and receives from r-stride;
+        -1 reverses (stride = ranks per group of a group-sharded level)."""
         if self.size == 1:
             return
         ops = []
-        dst, src = self.rank + direction, self.rank - direction
+        dst, src = self.rank + direction * stride, self.rank - direction * stride
         has_send = send is not None and 0 <= dst < self.size
         has_recv = recv is not None and 0 <= src < self.size
         s_buf = send.cpu() if (has_send and self.host_staged and send.is_cuda) else send
@@ -91,6 +105,16 @@ class Comm:
             return
         dist.all_gather_into_tensor(full, local.contiguous(), group=self.group)
 
+    def allgather_groups(self, full: torch.Tensor, local: torch.Tensor, stride: int):
+        """All-gather when consecutive blocks of `stride` ranks hold identical
+        slabs (one group): `full` receives one slab per group, in group order."""
+        if stride == 1:
+            self.allgather(full, local)
+            return
+        tmp = torch.empty((self.size,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+        self.allgather(tmp.view(self.size * local.shape[0], *local.shape[1:]), local)
+        full.copy_(tmp[::stride].reshape(full.shape))
+
 
 # ---------------------------------------------------------------------------
 # plan
@@ -100,10 +124,12 @@ class Comm:
 class LevelPlan:
     n_steps: int
     m: int | None          # coarsening factor toward the next level (None: coarsest)
-    sharded: bool
-    cb: int = 0            # first owned interval (sharded) / 0
+    sharded: bool          # split over groups > 1 rank groups (row exchanges needed)
+    cb: int = 0            # first owned interval of this rank's group
     ce: int = 0            # one past the last owned interval
     row0: int = 0          # global step of local row 0
+    groups: int = 1        # Q: rank groups the level is split over (P: fully sharded, 1: replicated)
+    stride: int = 1        # P / Q: ranks per group = rank distance between counterparts
 
     @property
     def n_intervals(self):
@@ -111,25 +137,27 @@ class LevelPlan:
 
     @property
     def local_rows(self):
-        return (self.ce - self.cb) * self.m + 1 if self.sharded else self.n_steps + 1
+        return (self.ce - self.cb) * self.m + 1 if self.m else self.n_steps + 1
 
 
 def make_plan(sizes: list[int], factors: list[int | None], rank: int, size: int) -> list[LevelPlan]:
-    """Shard each level while its interval count divides by P (and every finer
-    level is sharded); the remaining coarse levels are replicated."""
+    """Split level l's I_l intervals over Q_l = gcd(I_l, Q_{l-1}) rank groups
+    (Q_{-1} = P): Q = P shards a level fully, 1 < Q < P splits it over groups
+    of P/Q ranks, Q = 1 (and always the coarsest level) replicates it.  Q_l
+    divides Q_{l-1}, so each rank's finer C-indices lie in its coarse range."""
     plans = []
-    chain = True
+    q_prev = size
     for N, m in zip(sizes, factors):
         if m is None:
-            plans.append(LevelPlan(N, None, False))
+            plans.append(LevelPlan(N, None, False, 0, 0, 0, 1, size))
             continue
         I = N // m
-        chain = chain and I % size == 0
-        if chain:
-            cb, ce = rank * I // size, (rank + 1) * I // size
-            plans.append(LevelPlan(N, m, True, cb, ce, cb * m))
-        else:
-            plans.append(LevelPlan(N, m, False, 0, I, 0))
+        q = math.gcd(I, q_prev)
+        stride = size // q
+        w = rank // stride
+        cb, ce = w * I // q, (w + 1) * I // q
+        plans.append(LevelPlan(N, m, q > 1, cb, ce, cb * m, q, stride))
+        q_prev = q
     return plans
 
 
@@ -208,12 +236,17 @@ class TimeParallelCycle:
         self.U = [U0] + [z(p.local_rows) for p in plans[1:]]
         self.G = [None] + [z(p.local_rows) for p in plans[1:]]
         self.C = [z(p.ce - p.cb + 1) for p in plans[:-1]]
-        # restriction target of a sharded level whose child is replicated: a local
-        # slab (row 0 unused) that is all-gathered into the child's full G
+        # restriction target of a level whose child is split differently (fewer
+        # groups, or replicated): a local slab (row 0 unused), all-gathered
+        # per group into the child's rows 1..N_child, then the child's range
         self.Gslab = [None] * L
+        self.Gfull = [None] * L
         for li in range(L - 1):
-            if plans[li].sharded and not plans[li + 1].sharded:
-                self.Gslab[li] = z(plans[li].ce - plans[li].cb + 1)
+            p, c = plans[li], plans[li + 1]
+            if p.groups != c.groups:
+                self.Gslab[li] = z(p.ce - p.cb + 1)
+                if not (c.groups == 1 and p.stride == 1):
+                    self.Gfull[li] = z(c.n_steps)
         p0 = plans[0]
         self.partial = torch.zeros(p0.ce - p0.cb, dtype=dtype, device=device)
         self.partial_all = torch.zeros(p0.n_intervals, dtype=dtype, device=device)
@@ -225,8 +258,9 @@ class TimeParallelCycle:
         if phase in (_lib.PHASE_F_RES, _lib.PHASE_FONLY_RES):
             Gc = self.Gslab[li] if self.Gslab[li] is not None else self.G[li + 1]
         # the child's U/G local row 0 is global C-index c.row0 (== p.cb when both
-        # are sharded, 0 when the child is replicated); Uc is indexed from p.cb
-        Uc = self.U[li + 1] if c.sharded else self.U[li + 1][p.cb:]
+        # are split alike, the child group's first step otherwise); Uc is
+        # indexed from p.cb, which lies in the child's range
+        Uc = self.U[li + 1][p.cb - c.row0:]
         return dict(m=p.m, c_begin=p.cb, c_count=p.ce - p.cb, n_intervals=p.n_intervals, U=self.U[li],
                     u_row0=p.row0, G=self.G[li], g_row0=p.row0, Cbuf=self.C[li], Uc=Uc, Gc=Gc, c_row0=p.cb,
                     partial=self.partial if (li == 0 and phase == _lib.PHASE_INJ_F) else None, partial0=p.cb,
@@ -243,23 +277,34 @@ class TimeParallelCycle:
         if self.relax == "FCF":
             be.phase(li, _lib.PHASE_FC, **self._args(li, _lib.PHASE_FC, zero))
             if p.sharded:
-                comm.shift(self.C[li][last_local], self.C[li][0], +1)
+                comm.shift(self.C[li][last_local], self.C[li][0], +1, p.stride)
             be.phase(li, _lib.PHASE_F_RES, **self._args(li, _lib.PHASE_F_RES, zero))
         else:
             be.phase(li, _lib.PHASE_FONLY_RES, **self._args(li, _lib.PHASE_FONLY_RES, zero))
             if p.sharded:
-                comm.shift(self.C[li][last_local], self.C[li][0], +1)
+                comm.shift(self.C[li][last_local], self.C[li][0], +1, p.stride)
         if self.Gslab[li] is not None:
-            comm.allgather(self.G[li + 1][1:], self.Gslab[li][1:])
+            self._gather_restriction(li)
         self.cycle(li + 1)
         be.phase(li, _lib.PHASE_INJ_F, **self._args(li, _lib.PHASE_INJ_F, False))
         if p.sharded:
-            comm.shift(self.U[li][0], self.U[li][(p.ce - p.cb) * p.m], -1)
+            comm.shift(self.U[li][0], self.U[li][(p.ce - p.cb) * p.m], -1, p.stride)
+
+    def _gather_restriction(self, li: int):
+        """Child forcing rows from every group's C-residual slab."""
+        p, c = self.plans[li], self.plans[li + 1]
+        slab = self.Gslab[li][1:]
+        if self.Gfull[li] is None:        # fully sharded parent, replicated child
+            self.comm.allgather(self.G[li + 1][1:], slab)
+            return
+        full = self.Gfull[li]             # global child steps 1..N_child
+        self.comm.allgather_groups(full, slab, p.stride)
+        self.G[li + 1][1:].copy_(full[c.row0: c.row0 + c.local_rows - 1])
 
     def iteration(self):
         """One V-cycle, then the fine residual norm^2 (global order) into sumsq."""
         self.cycle(0)
-        self.comm.allgather(self.partial_all, self.partial)
+        self.comm.allgather_groups(self.partial_all, self.partial, self.plans[0].stride)
         self.be.total(self.partial_all, self.sumsq)
 
 
@@ -337,7 +382,7 @@ def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: boo
     levels[0]._apply(U, p0.row0, 1, nloc, R, U_sub=U[1:], row_sumsq=row_ss)
     del R
     row_all = torch.empty(cfg.n_t, dtype=torch.float64, device=dev)
-    comm.allgather(row_all, row_ss)
+    comm.allgather_groups(row_all, row_ss, p0.stride)
     s0 = torch.zeros(1, dtype=torch.float64, device=dev)
     be.total(row_all, s0)
     r0 = float(torch.sqrt(s0).item())

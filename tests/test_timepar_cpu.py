@@ -33,6 +33,12 @@ CASES = {
     "f_relax": dict(n_x=32, n_t=64, wave_speed="C3", p=1, schedule=4, relaxation="F"),
     "two_level_fixed": dict(n_x=32, n_t=64, wave_speed="C1", p=1, schedule=8, max_levels=2, iterate="pm1"),
 }
+# levels [32, 8, 2]: at P = 4 the fine level is fully sharded and level 1
+# (2 intervals) is split over 2 groups of 2 ranks
+GROUP_CASES = {
+    "group_split": dict(n_x=32, n_t=32, wave_speed="C3", p=3, schedule=4),
+    "group_split_f": dict(n_x=32, n_t=128, wave_speed="B2", p=1, schedule=8, relaxation="F", seed=2),
+}
 ITERS = 3
 
 
@@ -86,13 +92,25 @@ def _free_port():
 
 def test_plan_shards_and_replicates():
     plans = T.make_plan([4096, 1024, 256, 64, 16, 4], [4, 4, 4, 4, 4, None], 3, 8)
-    assert [p.sharded for p in plans] == [True, True, True, True, False, False]
+    # level 4 has 4 intervals: split over 4 groups of 2 ranks (rank 3 -> group 1)
+    assert [p.groups for p in plans] == [8, 8, 8, 8, 4, 1]
+    assert [p.sharded for p in plans] == [True, True, True, True, True, False]
+    assert (plans[4].stride, plans[4].cb, plans[4].ce, plans[4].row0, plans[4].local_rows) == (2, 1, 2, 4, 5)
     assert (plans[0].cb, plans[0].ce, plans[0].row0, plans[0].local_rows) == (384, 512, 1536, 513)
     # coarse rank-r rows are exactly the fine level's C-indices of rank r
     for f, c in zip(plans[:3], plans[1:4]):
         assert c.row0 == f.cb and c.local_rows == f.ce - f.cb + 1
+    # ... and a group-split child's range contains them
+    f, c = plans[3], plans[4]
+    assert c.row0 <= f.cb and f.ce <= c.row0 + c.local_rows - 1
     one = T.make_plan([64, 16, 4], [4, 4, None], 0, 1)
-    assert [p.sharded for p in one] == [True, True, False] and one[0].local_rows == 65
+    assert [p.sharded for p in one] == [False, False, False] and one[0].local_rows == 65
+    # cfg5 at P = 8: level 2 (4 intervals) over 4 groups, coarsest replicated
+    c5 = T.make_plan([2048, 256, 32, 4], [8, 8, 8, None], 5, 8)
+    assert [p.groups for p in c5] == [8, 8, 4, 1] and (c5[2].cb, c5[2].ce) == (2, 3)
+    # I not divisible by P: gcd groups (12 intervals over 8 ranks -> 4 groups)
+    odd = T.make_plan([48, 12, 3], [4, 4, None], 7, 8)
+    assert [p.groups for p in odd] == [4, 1, 1] and (odd[0].cb, odd[0].ce) == (9, 12)
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -117,3 +135,21 @@ def test_two_ranks_gloo_match_one_rank(tmp_path, name):
     assert np.array_equal(got["norms"], np.array(norms1))
     if name == "replicated_tail":
         assert list(got["sharded"]) == [True, False, False]
+
+
+@pytest.mark.parametrize("name", list(GROUP_CASES))
+def test_four_ranks_group_split_match_one_rank(tmp_path, name):
+    """A coarse level with fewer intervals than ranks is split over rank
+    groups (counterpart exchanges, grouped restriction all-gather): the
+    iterates and norms equal the single-rank engine's bit-for-bit."""
+    kw = GROUP_CASES[name]
+    ocfg = O.OConfig(**kw)
+    levels = O.hierarchy(ocfg)
+    plans = T.make_plan([lv.n_steps for lv in levels], [lv.cf for lv in levels[:-1]] + [None], 0, 4)
+    assert plans[0].groups == 4 and 1 < plans[1].groups < 4
+    out = str(tmp_path / "r.npz")
+    mp.spawn(_worker, args=(4, _free_port(), kw, out), nprocs=4, join=True)
+    got = np.load(out)
+    U1, _, norms1, _ = run_engine(kw, 0, 1)
+    assert np.array_equal(got["U"], U1)
+    assert np.array_equal(got["norms"], np.array(norms1))

@@ -21,6 +21,10 @@ CASES = {
     "1d_c3_frelax": dict(n_x=128, n_t=128, wave_speed="C3", p=1, schedule=4, relaxation="F"),
     "1d_replicated_tail": dict(n_x=128, n_t=96, wave_speed="C3", p=3, schedule=4),
     "2d_b4_p3_m4": dict(n_x=16, n_t=64, dim=2, wave_speed="B4", p=3, schedule=4, u0="sin4", seed=3),
+    # levels [32, 8, 2]: with 4 ranks level 1 (2 intervals) is split over 2
+    # rank groups (counterpart exchanges + grouped restriction all-gather)
+    "1d_group_split": dict(n_x=128, n_t=32, wave_speed="B2", p=3, schedule=4, seed=1),
+    "2d_group_split": dict(n_x=16, n_t=32, dim=2, wave_speed="B4", p=3, schedule=4, u0="sin4", seed=3),
 }
 
 
