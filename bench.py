@@ -174,16 +174,17 @@ def phase_bytes(level, phase, fine: bool) -> int:
     m = level.cf
     nI = N // m
     g = 0 if fine else 1           # G rows read (zero forcing on the fine level)
-    sig = 1 if level.kind != "fine" and level.sig_x is not None else 0
-    step = 8 * n * (1 + g + sig + 1)   # s + G + sigma + output row
+    d = level.grid.dim             # departure record and sigma: one fp64 per node per axis
+    sig = d if level.kind != "fine" and level.sig_x is not None else 0
+    step = 8 * n * (d + g + sig + 1)   # s + G + sigma + output row
     if phase == _lib.PHASE_FC:
         left = 0 if not fine else 8 * n
         return nI * (left + m * step)
     if phase == _lib.PHASE_F_RES:
-        per = 8 * n * 2 + (m - 1) * step + 8 * n * (1 + g + sig) + 8 * n * 3   # tail: s,G,sig + Cbuf r, U w, Gc w
+        per = 8 * n * 2 + (m - 1) * step + 8 * n * (d + g + sig) + 8 * n * 3   # tail: s,G,sig + Cbuf r, U w, Gc w
         return nI * per
     if phase == _lib.PHASE_INJ_F:
-        per = 8 * n * 3 + (m - 1) * step + (8 * n * (1 + g + sig) + 16 * n if fine else 0)
+        per = 8 * n * 3 + (m - 1) * step + (8 * n * (d + g + sig) + 16 * n if fine else 0)
         return nI * per
     return 0
 
@@ -291,18 +292,23 @@ def run_gpu(args):
             dist.barrier()
             dist.destroy_process_group()
         return
+    clk_summary = clk.summary()
     # ---- per-kernel breakdown of one single-GPU V-cycle (eager launches, CUDA events)
     breakdown, launches_iter = kernel_breakdown(levels, cfg)
     top = max(breakdown, key=lambda k: breakdown[k]["ms_total"])
     tb = breakdown[top]
     peak = _peak()
     achieved = tb["bytes"] / (tb["ms_avg"] / 1e3) / 1e9
-    limiter = ("latency: MGS-GMRES block-reduction chain (see DESIGN.md section 4)"
-               if "corrected" in top else "FP64 issue + HBM")
+    if "corrected" not in top:
+        limiter = "FP64 issue + HBM"
+    elif cfg.dim == 1:
+        limiter = "latency: MGS-GMRES reduction chain of a few row chains (see DESIGN.md section 4)"
+    else:
+        limiter = "per-system barriers + L2-resident Krylov passes of the cooperative GMRES (DESIGN.md section 4)"
     roofline = {"bound": "hbm", "limiter": limiter, "kernel": top, "achieved": round(achieved, 1),
                 "peak": peak["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peak["hbm_gbs"], 4),
-                "traffic": _ncu_traffic(top), "bytes_per_launch": tb["bytes"],
+                "traffic": _ncu_traffic(args.config, top), "bytes_per_launch": tb["bytes"],
                 "ms_per_launch": round(tb["ms_avg"], 5), "peak_source": peak["source"],
                 "share_of_iteration": round(tb["ms_total"] / sum(v["ms_total"] for v in breakdown.values()), 3)}
 
@@ -313,22 +319,41 @@ def run_gpu(args):
     if sl_key is not None:
         sb = breakdown[sl_key]
         ach = sb["bytes"] / (sb["ms_avg"] / 1e3) / 1e9
+        hbm_frac = ach / peak["hbm_gbs"]
         sl_roof = {"bound": "hbm", "kernel": sl_key, "achieved": round(ach, 1), "peak": peak["hbm_gbs"],
-                   "unit": "GB/s", "frac": round(ach / peak["hbm_gbs"], 4), "traffic": _ncu_traffic(sl_key),
+                   "unit": "GB/s", "frac": round(hbm_frac, 4), "traffic": _ncu_traffic(args.config, sl_key),
                    "bytes_per_launch": sb["bytes"], "ms_per_launch": round(sb["ms_avg"], 5),
-                   "note": "plain SL steps of the fine level; also FP64-issue bound (~32 FP64 ops per node-update)"}
+                   "note": "plain SL steps of the fine level (8 B record per axis + 8 B new row per node-update)"}
+        # the same launch against the FP64 issue rate: ncu-counted FP64
+        # instructions per node-update x node-updates / time
+        ops = _ncu_fp64(cfg.dim, cfg.p)
+        if ops:
+            lv0 = levels[0]
+            node_updates = lv0.n_steps * lv0.grid.n_points
+            sm_mhz = clk_summary.get("sm_mhz") or 1965.0
+            fpeak = 148 * 64 * sm_mhz * 1e6 / 1e12
+            fach = ops * node_updates / (sb["ms_avg"] / 1e3) / 1e12
+            sl_roof["fp64"] = {"achieved": round(fach, 2), "peak": round(fpeak, 2), "unit": "T FP64 inst/s",
+                               "frac": round(fach / fpeak, 4), "ops_per_node_update": ops,
+                               "source": "profiles/ncu_fp64.json (ncu SASS counts)"}
+            sl_roof["binding"] = "fp64" if fach / fpeak > hbm_frac else "hbm"
 
-    # ---- sequential GPU time stepping (fine level, one CTA walks all steps)
+    # ---- sequential GPU time stepping of the fine level (the sweep behind
+    #      P.sequential_reference: 1D one CTA walks all steps, 2D one batched
+    #      launch per step); state buffer and u0 prepared outside the timing
+    Useq = torch.empty((cfg.n_t + 1, npts), dtype=torch.float64, device="cuda")
+    Useq[0] = torch.from_numpy(M.initial_state(cfg, levels[0].grid)).cuda()
     for _ in range(2):
-        P.sequential_reference(cfg, levels, output="device")
+        M._sweep(levels[0], Useq, None, zero_init=False)
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
     for _ in range(3):
-        P.sequential_reference(cfg, levels, output="device")
+        M._sweep(levels[0], Useq, None, zero_init=False)
     s1.record()
     torch.cuda.synchronize()
     seq_ms = s0.elapsed_time(s1) / 3
+    del Useq
 
     iters = rep.iterations
     launches = 3 + 2 + launches_iter * iters      # pcg fill + r0 (rows + sum) + per-iteration
@@ -361,7 +386,7 @@ def run_gpu(args):
             "e2e": {"value": n_dof / (e2e / 1e3), "unit": "DOF/s", "ms_per_step": e2e,
                     "h2d_bytes_per_step": int(Xp.numel() * 8 + npts * 8) * world,
                     "d2h_bytes_per_step": int(Uh.numel() * 8) * world},
-            "clocks": clk.summary(),
+            "clocks": clk_summary,
             "gpu_launches": launches,
             "sequential_gpu_ms": round(seq_ms, 3),
             "speedup_vs_sequential_gpu": round(seq_ms / ms, 4),
@@ -441,14 +466,23 @@ def _peak():
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def _ncu_traffic(kernel_key):
+def _ncu_fp64(dim, p):
+    """FP64 instructions per node-update of the fine SL kernel (ncu-measured)."""
+    path = os.path.join(ROOT, "profiles", "ncu_fp64.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f).get(f"{dim}d_p{p}")
+
+
+def _ncu_traffic(config, kernel_key):
     """DRAM bytes per launch from the committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get(kernel_key)
+    return d.get(f"{config}:{kernel_key}")
 
 
 # ---------------------------------------------------------------------------
