@@ -218,6 +218,34 @@ int mgrit_axpy_rows(double *U, int64_t ldu, int64_t u_stride_rows,
                     const double *X, int64_t ldx, int64_t rows, int64_t n,
                     void *stream);
 
+/* ------------------------------------------- device-resident solve loop --- */
+
+/* The iteration loop of solve() (mgrit.py:355-373) as one CUDA graph: a WHILE
+ * node whose body is the captured V-cycle (the caller's launches between
+ * mgrit_loop_begin and mgrit_loop_end on `stream`) followed by the stop test
+ * (mgrit_loop_check).  Per solve: mgrit_loop_init (r0 from the initial
+ * residual's sum of squares), mgrit_loop_launch, one host sync, then read
+ *   ctrl[0] = iterations, ctrl[1] = MGRIT_LOOP_* state, hist[0..ctrl[0]].
+ * Stop rule, in the reference's order: non-finite GMRES input (status != 0)
+ * -> history NaN, diverged; r = sqrt(sumsq); !finite(r) or
+ * r >= divergence_factor*r0 -> diverged; r <= rtol*r0 -> converged;
+ * iterations == max_iters -> max_iters.
+ * ctrl: device int32[4]; par: device double[2] (written by mgrit_loop_init);
+ * hist: device double[max_iters + 1].  `stream` must not be the legacy
+ * default stream (it cannot be captured). */
+enum { MGRIT_LOOP_RUNNING = 0, MGRIT_LOOP_CONVERGED = 1, MGRIT_LOOP_DIVERGED = 2,
+       MGRIT_LOOP_MAX_ITERS = 3 };
+
+int mgrit_loop_begin(void *stream, void **loop_out);
+int mgrit_loop_check(void *loop, const double *sumsq, const int32_t *status,
+                     double *hist, int32_t *ctrl, const double *par, void *stream);
+int mgrit_loop_end(void *loop, void *stream);
+int mgrit_loop_init(const double *r0_sumsq, double *hist, int32_t *ctrl, double *par,
+                    double rtol, double divergence_factor, int32_t max_iters,
+                    void *stream);
+int mgrit_loop_launch(void *loop, void *stream);
+void mgrit_loop_destroy(void *loop);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,7 +70,15 @@ _SIGS = {
                                               c_vp, c_vp, c_i64, c_vp, c_vp]),
     "mgrit_sum": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
     "mgrit_axpy_rows": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp]),
+    "mgrit_loop_begin": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "mgrit_loop_check": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "mgrit_loop_end": (ctypes.c_int, [c_vp, c_vp]),
+    "mgrit_loop_init": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_i32, c_vp]),
+    "mgrit_loop_launch": (ctypes.c_int, [c_vp, c_vp]),
+    "mgrit_loop_destroy": (None, [c_vp]),
 }
+
+LOOP_STATES = {0: "running", 1: "converged", 2: "diverged", 3: "max_iters"}
 
 EXPORTED = tuple(_SIGS)
 

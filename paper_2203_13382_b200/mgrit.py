@@ -685,7 +685,7 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
         raise ValueError("fused engine needs a hierarchy without ideal levels")
     sess = _session(levels, cfg, dev) if use_fused else None
     U = sess.U if sess is not None else torch.empty((cfg.n_t + 1, n), dtype=torch.float64, device=dev)
-    U[0] = torch.from_numpy(initial_state(cfg, grid)).to(dev)
+    U[0] = _initial_row(cfg, fine, dev)
     if initial_iterate is not None:
         src = torch.as_tensor(initial_iterate)
         U[1:].copy_(src.reshape(cfg.n_t, n), non_blocking=True)
@@ -698,20 +698,28 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
     # only the per-row sums of squares are produced (no residual array)
     row_ss = sess.row_ss if sess is not None else torch.empty(cfg.n_t, dtype=torch.float64, device=dev)
     fine._apply(U, 0, 1, cfg.n_t, None, U_sub=U[1:], row_sumsq=row_ss)
-    r0 = float(torch.sqrt(device_sum(row_ss)).item())
-    history = [r0]
+    r0_ss = device_sum(row_ss)
     state = "max_iters"
     G0 = torch.zeros_like(U) if not use_fused else None
 
-    if use_fused:
+    if use_fused and use_graph:
+        # device-resident loop: one graph launch, one host sync per solve
+        loop = _solve_loop(sess, cfg, status)
+        lib = _lib.load()
+        _lib.check(lib.mgrit_loop_init(r0_ss.data_ptr(), loop.hist.data_ptr(), loop.ctrl.data_ptr(),
+                                       loop.par.data_ptr(), float(cfg.rtol), float(cfg.divergence_factor),
+                                       int(cfg.max_iters), stream_ptr()), "loop_init")
+        _lib.check(lib.mgrit_loop_launch(loop.handle, stream_ptr()), "loop_launch")
+        ctrl = loop.ctrl.cpu()
+        k = int(ctrl[0])
+        state = _lib.LOOP_STATES[int(ctrl[1])]
+        history = loop.hist[:k + 1].cpu().tolist()
+    elif use_fused:
+        history = [float(torch.sqrt(r0_ss).item())]
+        r0 = history[0]
         eng = sess.engine
         for it in range(cfg.max_iters):
-            if sess.graph is not None and use_graph:
-                sess.graph.replay()
-            else:
-                eng.iteration()
-                if use_graph and cfg.max_iters > 1:
-                    sess.graph = _capture(eng.iteration)
+            eng.iteration()
             ss = float(eng.sumsq.item())
             bad = int(status.item())
             if bad:
@@ -727,6 +735,8 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
                 state = "converged"
                 break
     else:
+        history = [float(torch.sqrt(r0_ss).item())]
+        r0 = history[0]
         for _ in range(cfg.max_iters):
             try:
                 v_cycle(levels, 0, U, G0, cfg.relaxation)
@@ -762,12 +772,68 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
 @dataclass
 class _Session:
     """Per-hierarchy solve workspace: the state buffer, the fused engine and
-    its captured CUDA graph survive across solve() calls on the same levels."""
+    its captured solve loop survive across solve() calls on the same levels."""
 
     U: torch.Tensor
     row_ss: torch.Tensor
     engine: "_FusedCycle"
-    graph: object = None
+    loop: "_Loop | None" = None
+
+
+class _Loop:
+    """The captured device-resident convergence loop (loop.cu): a CUDA graph
+    whose WHILE node runs one V-cycle + the stop test per pass."""
+
+    def __init__(self, handle, hist, ctrl, par):
+        self.handle, self.hist, self.ctrl, self.par = handle, hist, ctrl, par
+
+    def __del__(self):
+        if self.handle:
+            _lib.load().mgrit_loop_destroy(self.handle)
+            self.handle = None
+
+
+def _solve_loop(sess: _Session, cfg: SolverConfig, status: torch.Tensor) -> _Loop:
+    """Capture (once per session, again only if max_iters outgrows the
+    history buffer) the V-cycle + stop test into the body of a WHILE node."""
+    if sess.loop is not None and sess.loop.hist.numel() > cfg.max_iters:
+        return sess.loop
+    sess.loop = None
+    lib = _lib.load()
+    dev = sess.U.device
+    eng = sess.engine
+    hist = torch.zeros(max(cfg.max_iters, 100) + 1, dtype=torch.float64, device=dev)
+    ctrl = torch.zeros(4, dtype=torch.int32, device=dev)
+    par = torch.zeros(2, dtype=torch.float64, device=dev)
+    cur = torch.cuda.current_stream()
+    side = torch.cuda.Stream(device=dev)   # the legacy default stream cannot be captured
+    side.wait_stream(cur)
+    h = ctypes.c_void_p()
+    with torch.cuda.stream(side):
+        sp = stream_ptr()
+        _lib.check(lib.mgrit_loop_begin(sp, ctypes.byref(h)), "loop_begin")
+        try:
+            eng.iteration()
+            _lib.check(lib.mgrit_loop_check(h, eng.sumsq.data_ptr(), status.data_ptr(), hist.data_ptr(),
+                                            ctrl.data_ptr(), par.data_ptr(), sp), "loop_check")
+            _lib.check(lib.mgrit_loop_end(h, sp), "loop_end")
+        except Exception:
+            lib.mgrit_loop_destroy(h)
+            raise
+    cur.wait_stream(side)
+    sess.loop = _Loop(h, hist, ctrl, par)
+    return sess.loop
+
+
+def _initial_row(cfg: SolverConfig, fine: "Level", dev) -> torch.Tensor:
+    """U[0] = u0 on the grid (mgrit.py:352), computed on the host with numpy
+    (the reference's values, bit for bit) once per hierarchy and kept in HBM."""
+    cache = fine.__dict__.setdefault("_u0_rows", {})
+    row = cache.get(cfg.u0)
+    if row is None or row.device != dev:
+        row = torch.from_numpy(initial_state(cfg, fine.grid)).to(dev)
+        cache[cfg.u0] = row
+    return row
 
 
 def _session(levels, cfg, dev) -> _Session:
