@@ -591,7 +591,11 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
         const double nrm = sqrt(ar_recv<false>(cx, tn).x);
         MGRIT_PROBE_AT(413 + 6 * kk);
         const bool brk = nrm <= __dmul_rn(1e-14, beta);
-        if (!brk) {
+        // b_{kk+1} = w / h_{kk+1,kk}; written even on breakdown (the slot is
+        // then never read: the loop stops and x uses slots < kk + 1), so
+        // the normalisation and the rotation below form one basic block
+        // whose two dependent chains the scheduler can interleave
+        {
             const double yn = __drcp_rn(nrm);
 #pragma unroll
             for (int k = 0; k < NPT; ++k) v[k] = div_rcp(v[k], nrm, yn);
@@ -623,14 +627,15 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
         double acc = lane < done ? S.g[lane] : 0.0;
         const double hjj = lane < done ? S.H[lane * kMaxKrylov + lane] : 1.0;
         const double rjj = lane < done ? S.rdiag[lane] : 1.0;
-        // branch-free: steps j >= done give y_j = 0 / 1 = 0 and touch nothing
+        // steps j >= done are skipped (warp-uniform branch; y_j stays 0)
         double myy = 0.0;
 #pragma unroll
         for (int j = KM - 1; j >= 0; --j) {
+            if (j >= done) continue;
+            const bool upd = lane < j;
+            const double hlj = upd ? S.H[lane * kMaxKrylov + j] : 0.0;
             const double yj = __shfl_sync(0xffffffffu, div_rcp(acc, hjj, rjj), j);
             myy = lane == j ? yj : myy;
-            const bool upd = lane < j && j < done;
-            const double hlj = upd ? S.H[lane * kMaxKrylov + j] : 0.0;
             acc = upd ? __dsub_rn(acc, __dmul_rn(hlj, yj)) : acc;
         }
         if (lane < KM) S.y[lane] = myy;
@@ -640,17 +645,14 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
     MGRIT_PROBE_AT(484);
 #pragma unroll
     for (int k = 0; k < NPT; ++k) v[k] = 0.0;
-    // branch-free (slots j >= done may hold stale values: masked loads)
+    // j ascending over the done slots (uniform bound across the cluster)
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
-        const bool use = j < done;
+        if (j >= done) break;
         const double yj = S.y[j];
         const double *bj = cx.slot(j);
 #pragma unroll
-        for (int k = 0; k < NPT; ++k) {
-            const double b = use ? bj[tid + k * NTC] : 0.0;
-            v[k] = fma(b, yj, v[k]);
-        }
+        for (int k = 0; k < NPT; ++k) v[k] = fma(bj[tid + k * NTC], yj, v[k]);
     }
     MGRIT_PROBE_AT(481);
     return done;

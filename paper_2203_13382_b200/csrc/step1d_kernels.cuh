@@ -314,21 +314,16 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 const double nrm = sqrt(block_sum2<NT>(sumsq4(), cx));
                 MGRIT_PROBE_AT(13 + 8 * kk);
                 const bool brk = nrm <= __dmul_rn(1e-14, beta);
-                if (!brk) {
-                    const double yn = 1.0 / nrm;
-                    double *bnv = cx.bvec(kk + 1, n);
-#pragma unroll
-                    for (int k = 0; k < NPT; ++k) {
-                        const int i = tid + k * NT;
-                        v[k] = div_rcp(v[k], nrm, yn);
-                        if (F || i < n) bnv[i] = v[k];
-                    }
-                }
-                MGRIT_PROBE_AT(14 + 8 * kk);
+                // b_{kk+1} = w / h_{kk+1,kk}, written even on breakdown (the
+                // slot is then never read), so no branch separates it from
+                // thread 0's rotation below
                 if (tid == 0) {
-                    // new rotation from (H[kk][kk], h_{kk+1,kk} = nrm)
+                    // new rotation from (H[kk][kk], h_{kk+1,kk} = nrm); the
+                    // divisions are reciprocal + Markstein correction
+                    // (correctly rounded, = hess / denom)
                     const double den = hypot(hrun, nrm);
-                    const double c = __ddiv_rn(hrun, den), sn = __ddiv_rn(nrm, den);
+                    const double rden = __drcp_rn(den);
+                    const double c = div_rcp(hrun, den, rden), sn = div_rcp(nrm, den, rden);
                     G.cs[kk] = c;
                     G.sn[kk] = sn;
                     G.H[kk * kMaxKrylov + kk] = den;
@@ -337,6 +332,17 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                     G.g[kk + 1] = gn;
                     g_k = gn;
                     G.stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta));
+                }
+                MGRIT_PROBE_AT(14 + 8 * kk);
+                {
+                    const double yn = __drcp_rn(nrm);
+                    double *bnv = cx.bvec(kk + 1, n);
+#pragma unroll
+                    for (int k = 0; k < NPT; ++k) {
+                        const int i = tid + k * NT;
+                        v[k] = div_rcp(v[k], nrm, yn);
+                        if (F || i < n) bnv[i] = v[k];
+                    }
                 }
                 MGRIT_PROBE_AT(15 + 8 * kk);
                 done = kk + 1;

@@ -115,9 +115,21 @@ __device__ __forceinline__ int64_t row_t(const Rows2D &a, int64_t b) {
     return a.t_idx ? a.t_idx[b] : a.t_first + b * a.t_stride;
 }
 
-// plain SL (SLONLY: write S only, no forcing / residual form)
-template <int P, bool SLONLY>
-__global__ void __launch_bounds__(kNT2) sl2d_kernel(mgrit_level_desc L, Rows2D a) {
+// plain SL (SLONLY: write S only, no forcing / residual form).
+// The step is FP64-issue bound with the tap gathers' L1 latency as the main
+// stall, so occupancy and early record loads matter: PREF loads the CTA
+// tile's departure records (streaming, read once per phase) before any
+// gather, and MINB caps registers for resident CTAs per SM.  Measured on
+// B200 per batched F-step (tools/sl2d_variants.py): p = 3 best at 8 CTAs/SM
+// (32 regs: cfg4 0.865 -> 0.713 ms), p = 5 at 4 CTAs/SM (64 regs: cfg5
+// 5.87 -> 4.99 ms); records loaded lazily were 4-18 % slower.
+template <int P>
+struct SL2DMinBlocks {
+    static constexpr int value = P == 5 ? 4 : 8;
+};
+
+template <int P, bool SLONLY, int MINB, bool PREF>
+__global__ void __launch_bounds__(kNT2, MINB) sl2d_kernel(mgrit_level_desc L, Rows2D a) {
     __shared__ double red[kNT2 / 32 + 1];
     const int nx = L.n_x;
     const int64_t n = L.n_points;
@@ -127,11 +139,21 @@ __global__ void __launch_bounds__(kNT2) sl2d_kernel(mgrit_level_desc L, Rows2D a
     const double *sx = L.s_x + set * n, *sy = L.s_y + set * n;
     const double *u = a.U_in + b * a.ld_in;
     double ss = 0.0;
+    constexpr int NK = kTile2 / kNT2;
+    double rx[PREF ? NK : 1], ry[PREF ? NK : 1];
+    if constexpr (PREF) {
 #pragma unroll
-    for (int k = 0; k < kTile2 / kNT2; ++k) {
+        for (int k = 0; k < NK; ++k) {
+            const int64_t i = (int64_t)blockIdx.x * kTile2 + k * kNT2 + threadIdx.x;
+            rx[k] = i < n ? __ldcs(sx + i) : 0.0;
+            ry[k] = i < n ? __ldcs(sy + i) : 0.0;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
         const int64_t i = (int64_t)blockIdx.x * kTile2 + k * kNT2 + threadIdx.x;
         if (i < n) {
-            double v = sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
+            double v = PREF ? sl2d_at<P>(u, nx, rx[k], ry[k]) : sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
             if constexpr (!SLONLY) {
                 const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
                 if (a.U_sub) {
@@ -609,14 +631,14 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             Rows2D s = a;
             s.out = V;
             s.ld_out = n;
-            sl2d_kernel<P, true><<<grid, kNT2, 0, st>>>(*L, s);
+            sl2d_kernel<P, true, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
             Rows2D f = a;
             f.partial = partial;
             fe2d_kernel<P><<<grid, kNT2, 0, st>>>(*L, f, V);
         } else {
             Rows2D s = a;
             s.partial = partial;
-            sl2d_kernel<P, false><<<grid, kNT2, 0, st>>>(*L, s);
+            sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
         }
         if (partial) rowsum_kernel<<<(unsigned)(r.B < 4096 ? r.B : 4096), kNT2, 0, st>>>(partial, tiles, r.B, r.row_sumsq);
         return check_launch("apply_rows_2d");
