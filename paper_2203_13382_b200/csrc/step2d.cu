@@ -100,6 +100,39 @@ __device__ __forceinline__ double imsd2d_at(const double *v, int nx, int ix, int
     return __dsub_rn(__dsub_rn(vi, __dmul_rn(sx, dx)), __dmul_rn(sy, dy));
 }
 
+// Same operator applied to b = v / s, each value of b formed exactly as the
+// normalisation b_j = w / h would store it (div_rcp, = RN(v / s)); also
+// returns b at the node itself.  Lets the GMRES stencil pass read the
+// un-normalised Arnoldi vector and write b_kk on the fly (no separate pass).
+template <int P>
+__device__ __forceinline__ double imsd2d_scaled(const double *v, int nx, int ix, int iy, double sx, double sy,
+                                                double s, double rs, double &bi) {
+    constexpr int RAD = (P + 1) / 2;
+    const double *row = v + (int64_t)iy * nx;
+    auto bq = [&](double x) { return div_rcp(x, s, rs); };
+    const double vi = bq(row[ix]);
+    bi = vi;
+    double dx = cmul<P>(RAD, vi), dy = cmul<P>(RAD, vi);
+    if (ix >= RAD && ix + RAD < nx && iy >= RAD && iy + RAD < nx) {
+        const double *c = row + ix;
+#pragma unroll
+        for (int q = 1; q <= RAD; ++q) {
+            dx = __dadd_rn(__dadd_rn(dx, cmul<P>(RAD + q, bq(c[q]))), cmul<P>(RAD - q, bq(c[-q])));
+            dy = __dadd_rn(__dadd_rn(dy, cmul<P>(RAD + q, bq(c[(int64_t)q * nx]))),
+                           cmul<P>(RAD - q, bq(c[-(int64_t)q * nx])));
+        }
+        return __dsub_rn(__dsub_rn(vi, __dmul_rn(sx, dx)), __dmul_rn(sy, dy));
+    }
+#pragma unroll
+    for (int q = 1; q <= RAD; ++q) {
+        dx = __dadd_rn(__dadd_rn(dx, cmul<P>(RAD + q, bq(row[wrapi(ix + q, nx)]))),
+                       cmul<P>(RAD - q, bq(row[wrapi(ix - q, nx)])));
+        dy = __dadd_rn(__dadd_rn(dy, cmul<P>(RAD + q, bq(v[(int64_t)wrapi(iy + q, nx) * nx + ix]))),
+                       cmul<P>(RAD - q, bq(v[(int64_t)wrapi(iy - q, nx) * nx + ix])));
+    }
+    return __dsub_rn(__dsub_rn(vi, __dmul_rn(sx, dx)), __dmul_rn(sy, dy));
+}
+
 struct Rows2D {
     int64_t B;
     const int64_t *t_idx;
@@ -234,7 +267,8 @@ struct Coop2D {
     int chunks;               // CTAs per system
     int64_t nwb;              // warp blocks per system
     double *basis;            // [rows_per_round][K+1][n]
-    double *w;                // [rows_per_round][n]
+    double *w;                // [rows_per_round][n] Arnoldi vector (ping)
+    double *w2;               // [rows_per_round][n] Arnoldi vector (pong)
     double *part;             // [2][rows_per_round][nwb] reduction partials
     int *flags;               // [rows_per_round][chunks] non-finite rhs
     unsigned int *bar;        // [rows_per_round] per-system barrier counters (zeroed per launch)
@@ -354,7 +388,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     if (!active_cta) return;
 
     double *basis = C.basis + (int64_t)slot * (K + 1) * n;
-    double *w = C.w + (int64_t)slot * n;
+    double *const wping = C.w + (int64_t)slot * n, *const wpong = C.w2 + (int64_t)slot * n;
     for (int64_t b = slot; b < a.B; b += C.rows_per_round) {
         const int64_t t = row_t(a, b);
         const int64_t set = L.shared ? 0 : t;
@@ -362,11 +396,12 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
         const double *gx = L.sig_x + set * n, *gy = L.sig_y + set * n;
         // ---- SL rhs into w, non-finite flag, beta
         int bad = 0;
+        double *src = wping, *dst = wpong;   // Arnoldi vector: read / written by the stencil pass
         {
             const double *u = a.U_in + b * a.ld_in;
             for_nodes_red([&](int64_t i, int ix, int iy) {
                 const double v = sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
-                w[i] = v;
+                src[i] = v;
                 if (!isfinite(v)) bad = 1;
                 return __dmul_rn(v, v);
             });
@@ -381,25 +416,29 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
         int done = 0;
         const bool skip = anybad || beta == 0.0;
         if (anybad && tid == 0 && chunk == 0) atomicExch(C.status, 1);
-        if (!skip) {
-            const double yb = 1.0 / beta;
-            for_nodes([&](int64_t i, int ix, int iy) { basis[i] = div_rcp(w[i], beta, yb); });
-        }
         if (tid == 0) S.stop = skip ? 1 : 0;
         double g_k = beta;
+        // b_kk = src / scale is never stored by a pass of its own: the stencil
+        // pass of iteration kk forms it on the fly from src (every value
+        // exactly as the normalisation would store it), writes the node's own
+        // b_kk, and writes w = A b_kk into dst.  src was completed before the
+        // system barrier inside the gtotal() that produced `scale`.
+        double scale = beta, rscale = 1.0 / beta;
         // the stop test is evaluated from the same totals in every CTA of the
         // system, so all of them leave the loop at the same kk
         for (int kk = 0; kk < K; ++kk) {
             __syncthreads();
             if (S.stop) break;
-            ssync();  // b_kk complete in every chunk (the stencil reads across chunks)
-            const double *bk = basis + (int64_t)kk * n;
-            // w = A b_kk ; inner product with b_0
+            double *bk = basis + (int64_t)kk * n;
+            // b_kk, w = A b_kk ; inner product with b_0
             for_nodes_red([&](int64_t i, int ix, int iy) {
-                const double x = imsd2d_at<P>(bk, nx, ix, iy, __ldg(gx + i), __ldg(gy + i));
-                w[i] = x;
-                return __dmul_rn(basis[i], x);
+                double bi;
+                const double x = imsd2d_scaled<P>(src, nx, ix, iy, __ldg(gx + i), __ldg(gy + i), scale, rscale, bi);
+                bk[i] = bi;
+                dst[i] = x;
+                return __dmul_rn(kk == 0 ? bi : basis[i], x);
             });
+            double *const w = dst;
             double hrun = 0.0;
             for (int j = 0; j <= kk; ++j) {
                 const double h = gtotal();
@@ -432,11 +471,11 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             }
             const double nrm = sqrt(gtotal());
             const bool brk = nrm <= __dmul_rn(1e-14, beta);
-            if (!brk) {
-                const double yn = 1.0 / nrm;
-                double *bn = basis + (int64_t)(kk + 1) * n;
-                for_nodes([&](int64_t i, int ix, int iy) { bn[i] = div_rcp(w[i], nrm, yn); });
-            }
+            // b_{kk+1} = w / nrm is formed by the next stencil pass
+            scale = nrm;
+            rscale = 1.0 / nrm;
+            dst = src;
+            src = w;
             if (tid == 0) {
                 const double den = hypot(hrun, nrm);
                 const double c = __ddiv_rn(hrun, den), sn = __ddiv_rn(nrm, den);
@@ -538,7 +577,7 @@ static int64_t coop_rows_cap(const mgrit_level_desc *L) {
 
 static int64_t coop_row_bytes(const mgrit_level_desc *L) {
     const int64_t n = L->n_points, nwb = (n + kWB - 1) / kWB;
-    return 8 * ((int64_t)(L->gmres_max_iters + 2) * n + 2 * nwb) + 4 * 4096 + 8;
+    return 8 * ((int64_t)(L->gmres_max_iters + 3) * n + 2 * nwb) + 4 * 4096 + 8;
 }
 
 int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows) {
@@ -596,7 +635,8 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             C.nwb = nwb;
             C.basis = (double *)scr;
             C.w = C.basis + rows * (int64_t)(L->gmres_max_iters + 1) * n;
-            C.part = C.w + rows * n;
+            C.w2 = C.w + rows * n;
+            C.part = C.w2 + rows * n;
             C.flags = (int *)(C.part + 2 * rows * nwb);
             C.bar = (unsigned int *)(C.flags + rows * chunks);
             if (cudaMemsetAsync(C.bar, 0, rows * sizeof(unsigned int), st) != cudaSuccess) {
