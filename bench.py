@@ -572,7 +572,7 @@ def main():
     ap.add_argument("--cpu-samples", type=int, default=1)
     ap.add_argument("--gmres-variant", default="mgs", choices=["mgs", "mgs_lowsync"],
                     help="coarse-level Arnoldi orthogonalisation (mgs = the reference's loop)")
-    ap.add_argument("--launch-policy", default="auto", choices=["auto", "cta", "cluster"],
+    ap.add_argument("--launch-policy", default="auto", choices=["auto", "cta", "cluster", "auto_one"],
                     help="corrected 1D kernels: one CTA or one 8-SM cluster per row chain")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     args = ap.parse_args()

@@ -35,7 +35,8 @@ extern "C" {
 enum { MGRIT_OK = 0, MGRIT_EINVAL = 2, MGRIT_ECUDA = 3 };
 /* launch policy of corrected 1D phases / sweeps: AUTO picks the cluster-split
  * kernels when the level has too few row chains to fill the GPU */
-enum { MGRIT_LAUNCH_AUTO = 0, MGRIT_LAUNCH_CTA = 1, MGRIT_LAUNCH_CLUSTER = 2 };
+enum { MGRIT_LAUNCH_AUTO = 0, MGRIT_LAUNCH_CTA = 1, MGRIT_LAUNCH_CLUSTER = 2,
+       MGRIT_LAUNCH_AUTO_ONE = 3 /* AUTO without the two-CTAs-per-SM phase form */ };
 
 /* operator kinds (mgrit.py:34).  MGRIT_KIND_SL covers "fine" and
  * "rediscretized" (plain semi-Lagrangian step); "ideal" is composed on the

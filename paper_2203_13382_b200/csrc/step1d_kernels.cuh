@@ -109,7 +109,7 @@ __device__ __forceinline__ void load_records(const mgrit_level_desc &L, int64_t 
 // Returns the GMRES Arnoldi count for corrected kinds (-1 on non-finite rhs),
 // 0 otherwise.  rowbuf is clobbered for KIND != SL; the caller must
 // __syncthreads() before rewriting it.
-template <int P, int KIND, int NT, int NPT, bool F, bool NUMBA>
+template <int P, int KIND, int NT, int NPT, bool F, bool NUMBA, bool LOWREG = false>
 __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, double (&v)[NPT],
                          const double (&sv)[NPT]) {
     constexpr int SL = Stencil<P>::L;
@@ -140,7 +140,8 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
         return 0;
     } else {
         constexpr int RAD = (P + 1) / 2;
-        constexpr bool SIGREG = NPT <= 8 || NT <= 256;
+        // sigma in registers unless the kernel runs two CTAs per SM (LOWREG)
+        constexpr bool SIGREG = !LOWREG && (NPT <= 8 || NT <= 256);
         const int64_t set = L.shared ? 0 : t;
         const double *sig = L.sig_x + set * (int64_t)n;
         double sg[SIGREG ? NPT : 1];
@@ -270,7 +271,19 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 // one MGS step on (cur = b_j in registers); nxt receives b_{j+1}
                 // (loads issued first so they overlap the FMAs and the reduction)
                 auto mgs_step = [&](int j, double (&cur)[NPT], double (&nxt)[NPT]) {
-                    if (j < kk) {
+                    if constexpr (LOWREG) {
+                        // no register prefetch of b_{j+1} (register budget of two
+                        // CTAs per SM): load b_j here; the co-resident CTA hides
+                        // the shared-memory latency
+                        if (j > 0) {
+                            const double *bp = j == kk ? cx.rowbuf : cx.bvec(j, n);
+#pragma unroll
+                            for (int k = 0; k < NPT; ++k) {
+                                const int i = tid + k * NT;
+                                cur[k] = (F || i < n) ? bp[i] : 0.0;
+                            }
+                        }
+                    } else if (j < kk) {
                         const double *bp = j + 1 == kk ? cx.rowbuf : cx.bvec(j + 1, n);
 #pragma unroll
                         for (int k = 0; k < NPT; ++k) {
@@ -304,11 +317,16 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                     for (int k = 0; k < NPT; ++k) v[k] = fma(-h, cur[k], v[k]);
                     if (kk == 5) MGRIT_PROBE_AT(303 + 4 * j);
                 };
-                double bo[NPT];
+                if constexpr (LOWREG) {
 #pragma unroll 1
-                for (int j = 0; j <= kk; j += 2) {
-                    mgs_step(j, bc, bo);
-                    if (j + 1 <= kk) mgs_step(j + 1, bo, bc);
+                    for (int j = 0; j <= kk; ++j) mgs_step(j, bc, bc);
+                } else {
+                    double bo[NPT];
+#pragma unroll 1
+                    for (int j = 0; j <= kk; j += 2) {
+                        mgs_step(j, bc, bo);
+                        if (j + 1 <= kk) mgs_step(j + 1, bo, bc);
+                    }
                 }
                 MGRIT_PROBE_AT(12 + 8 * kk);
                 const double nrm = sqrt(block_sum2<NT>(sumsq4(), cx));
@@ -502,9 +520,9 @@ __global__ void __launch_bounds__(NT, 1) rows_kernel(mgrit_level_desc L, RowsArg
 // ---------------------------------------------------------------------------
 // fused level phases: one CTA per C-interval (persistent over intervals)
 
-template <int P, int KIND, int NT, int NPT, bool F>
-__global__ void __launch_bounds__(NT, 1) phase_kernel(mgrit_level_desc L, mgrit_phase_args A, int nbs,
-                                                   double *scratch, int32_t *status) {
+template <int P, int KIND, int NT, int NPT, bool F, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) phase_kernel(mgrit_level_desc L, mgrit_phase_args A, int nbs,
+                                                      double *scratch, int32_t *status) {
     extern __shared__ double sm[];
     // The next step's departure records are prefetched into registers while
     // the current step computes (plain SL and small NPT; register prefetch
@@ -576,7 +594,7 @@ __global__ void __launch_bounds__(NT, 1) phase_kernel(mgrit_level_desc L, mgrit_
             if constexpr (PREFETCH) {
                 if (k < kmax) load_records<NT, NPT, F>(L, t, sn);
             }
-            cta_apply<P, KIND, NT, NPT, F, false>(L, t - 1, cx, v, sv);
+            cta_apply<P, KIND, NT, NPT, F, false, (MINB > 1)>(L, t - 1, cx, v, sv);
             if constexpr (PREFETCH) {
 #pragma unroll
                 for (int q = 0; q < NPT; ++q) sv[q] = sn[q];
@@ -730,6 +748,18 @@ inline int smem_slots(const mgrit_level_desc *L) {
     return (int)(k < 0 ? 0 : k);
 }
 
+// Krylov slots that fit when two CTAs share an SM (half of the SM's shared
+// memory each, less the per-CTA reservation)
+inline int smem_slots_two(const mgrit_level_desc *L) {
+    int dev = 0, per_sm = 228 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const int64_t avail = per_sm / 2 - 1024 - (int64_t)smem_bytes_for(L->n_x, 0);
+    int64_t k = avail > 0 ? avail / ((int64_t)L->n_x * 8) : 0;
+    if (k > L->gmres_max_iters + 1) k = L->gmres_max_iters + 1;
+    return (int)(k < 0 ? 0 : k);
+}
+
 inline int resident_ctas(const void *fn, int nt, size_t smem) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
@@ -756,6 +786,13 @@ template <int P_, int KIND_, int NT_, int NPT_, bool F_>
 struct Tag {
     static constexpr int P = P_, KIND = KIND_, NT = NT_, NPT = NPT_;
     static constexpr bool F = F_;  // n == NT * NPT: no bounds checks
+};
+
+// corrected phases of 4096-node rows (256 threads x 16 nodes) also come in a
+// two-CTAs-per-SM form (<= 128 registers, half the shared memory)
+template <typename C>
+struct TwoPerSM {
+    static constexpr bool value = C::KIND == MGRIT_KIND_CORRECTED && C::NT == 256 && C::NPT == 16 && C::F;
 };
 
 // full rows (n == NT*NPT: the power-of-two meshes of every BASELINE config)
@@ -835,7 +872,17 @@ int64_t Launch1D<P, KIND>::capacity(const mgrit_level_desc *L) {
         using C = decltype(T);
         auto fn = rows_kernel<C::P, C::KIND, C::NT, C::NPT, C::F>;
         if (prep(fn, smem)) return 1;
-        return resident_ctas((const void *)fn, C::NT, smem);
+        int cap = resident_ctas((const void *)fn, C::NT, smem);
+        if constexpr (TwoPerSM<C>::value) {
+            // the phase kernel's two-CTAs-per-SM form (scratch is sized from this)
+            const size_t smem2 = smem_bytes_for(L->n_x, smem_slots_two(L));
+            auto fn2 = phase_kernel<C::P, C::KIND, C::NT, C::NPT, C::F, 2>;
+            if (!prep(fn2, smem2)) {
+                const int cap2 = resident_ctas((const void *)fn2, C::NT, smem2);
+                if (cap2 > cap) cap = cap2;
+            }
+        }
+        return cap;
     });
 }
 
@@ -881,7 +928,30 @@ int Launch1D<P, KIND>::phase(const mgrit_level_desc *L, const mgrit_phase_args *
         auto fn = phase_kernel<C::P, C::KIND, C::NT, C::NPT, C::F>;
         int r = prep(fn, smem);
         if (r) return r;
-        const int grid = cap_grid(A->c_count, resident_ctas((const void *)fn, C::NT, smem), L, scratch_bytes);
+        const int res1 = resident_ctas((const void *)fn, C::NT, smem);
+        if constexpr (TwoPerSM<C>::value) {
+            // more row chains than SMs: two CTAs per SM (fewer shared-memory
+            // Krylov slots, sigma re-read from L1) finish them in one wave
+            // instead of two; the chains are latency bound, so two per SM
+            // overlap their reduction chains
+            if (A->c_count > res1 && L->launch_policy != MGRIT_LAUNCH_AUTO_ONE) {
+                const int nbs2 = smem_slots_two(L);
+                const size_t smem2 = smem_bytes_for(L->n_x, nbs2);
+                auto fn2 = phase_kernel<C::P, C::KIND, C::NT, C::NPT, C::F, 2>;
+                if ((r = prep(fn2, smem2))) return r;
+                int64_t g = A->c_count;
+                const int res2 = resident_ctas((const void *)fn2, C::NT, smem2);
+                if (g > res2) g = res2;
+                const int spill = L->gmres_max_iters + 1 - nbs2;
+                const int64_t per = spill > 0 ? (int64_t)spill * L->n_x * 8 : 0;
+                if (per > 0 && scratch_bytes / per < g) g = scratch_bytes / per;
+                if (g > res1) {
+                    fn2<<<(int)g, C::NT, smem2, st>>>(*L, *A, nbs2, (double *)scratch, status);
+                    return (int)MGRIT_OK;
+                }
+            }
+        }
+        const int grid = cap_grid(A->c_count, res1, L, scratch_bytes);
         if (grid < 1) return (int)MGRIT_EINVAL;
         fn<<<grid, C::NT, smem, st>>>(*L, *A, nbs, (double *)scratch, status);
         return (int)MGRIT_OK;

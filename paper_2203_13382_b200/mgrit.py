@@ -36,7 +36,7 @@ _KIND_CODE = {"fine": _lib.KIND_SL, "rediscretized": _lib.KIND_SL, "corrected": 
 
 
 GMRES_VARIANTS = ("mgs", "mgs_lowsync")
-LAUNCH_POLICIES = {"auto": 0, "cta": 1, "cluster": 2}
+LAUNCH_POLICIES = {"auto": 0, "cta": 1, "cluster": 2, "auto_one": 3}
 _launch_policy = "auto"
 
 
