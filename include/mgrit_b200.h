@@ -36,7 +36,10 @@ enum { MGRIT_OK = 0, MGRIT_EINVAL = 2, MGRIT_ECUDA = 3 };
 /* launch policy of corrected 1D phases / sweeps: AUTO picks the cluster-split
  * kernels when the level has too few row chains to fill the GPU */
 enum { MGRIT_LAUNCH_AUTO = 0, MGRIT_LAUNCH_CTA = 1, MGRIT_LAUNCH_CLUSTER = 2,
-       MGRIT_LAUNCH_AUTO_ONE = 3 /* AUTO without the two-CTAs-per-SM phase form */ };
+       MGRIT_LAUNCH_AUTO_ONE = 3, /* AUTO without the two-CTAs-per-SM phase form */
+       /* cluster kernels of exactly 2 / 4 / 8 / 16 CTAs wherever eligible */
+       MGRIT_LAUNCH_CLUSTER2 = 4, MGRIT_LAUNCH_CLUSTER4 = 5, MGRIT_LAUNCH_CLUSTER8 = 6,
+       MGRIT_LAUNCH_CLUSTER16 = 7 };
 
 /* operator kinds (mgrit.py:34).  MGRIT_KIND_SL covers "fine" and
  * "rediscretized" (plain semi-Lagrangian step); "ideal" is composed on the
@@ -76,7 +79,7 @@ typedef struct mgrit_level_desc {
                                the one-CTA kernels always run classic MGS, whose
                                block reductions are cheaper there) */
     int32_t launch_policy;  /* MGRIT_LAUNCH_*: corrected 1D levels may run one
-                               thread-block cluster (8 SMs) per row chain */
+                               thread-block cluster (2-16 SMs) per row chain */
 } mgrit_level_desc;
 
 /* ERK tableau for departure tracing (semi_lagrangian.py:46-72); built on the

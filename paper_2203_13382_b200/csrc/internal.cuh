@@ -23,7 +23,8 @@ int level_phase_1d(const mgrit_level_desc *L, const mgrit_phase_args *A, void *s
 int sweep_1d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg,
              int zero_init, int32_t *gmres_iters, void *scratch, int64_t scratch_bytes,
              int32_t *status, cudaStream_t st);
-int64_t rows_capacity(const mgrit_level_desc *L);
+int64_t rows_capacity(const mgrit_level_desc *L);      // incl. the two-CTAs-per-SM phase form
+int64_t rows_capacity_one(const mgrit_level_desc *L);  // one-CTA-per-SM forms only
 // cluster-split corrected 1D kernels; return -1 when not applicable
 int cl_level_phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int32_t *status, cudaStream_t st);
 int cl_sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg, int zero_init,

@@ -25,7 +25,12 @@ static int dispatch_pk(int p, int kind, F &&f) {
 
 int64_t rows_capacity(const mgrit_level_desc *L) {
     if (validate(L)) return 0;
-    return dispatch_pk(L->p, L->kind, [&](auto X) { return (int)decltype(X)::capacity(L); });
+    return dispatch_pk(L->p, L->kind, [&](auto X) { return (int)decltype(X)::capacity(L, false); });
+}
+
+int64_t rows_capacity_one(const mgrit_level_desc *L) {
+    if (validate(L)) return 0;
+    return dispatch_pk(L->p, L->kind, [&](auto X) { return (int)decltype(X)::capacity(L, true); });
 }
 
 int apply_rows_1d(const mgrit_level_desc *L, const RowsArgs &a, void *scratch,

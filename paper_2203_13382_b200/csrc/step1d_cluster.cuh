@@ -26,10 +26,12 @@
 namespace mgrit {
 namespace cl {
 
-constexpr int CS = 8;          // CTAs per cluster (portable maximum)
+// CS (CTAs per cluster: 2, 4, 8 portable; 16 non-portable) is a template
+// parameter of everything below; the launch policy picks it per level.
 constexpr int NTC = 128;       // threads per CTA
 constexpr int NWC = NTC / 32;  // warps per CTA
 constexpr int kNV = 32;        // values of one fused multi-reduction (d_0..15, gram_0..15)
+constexpr int kMaxKrylovCl = 10;  // Arnoldi steps unrolled at compile time (GmresConfig.max_iters)
 
 // ---------------------------------------------------------------- PTX ----
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -84,6 +86,7 @@ __device__ __forceinline__ void bulk_multicast(uint32_t dst, const void *src, ui
 }
 
 // ------------------------------------------------------- shared memory ----
+template <int CS>
 struct __align__(16) ClSmem {
     uint64_t rbar[2];   // receive mbarriers, used alternately by successive reductions
     uint64_t rowbar;    // full-row arrival (TMA multicast)
@@ -100,8 +103,9 @@ struct __align__(16) ClSmem {
     int stop;
 };
 
+template <int CS>
 struct ClCtx {
-    ClSmem *S;
+    ClSmem<CS> *S;
     double *row;     // full state row (global node index), halo kHalo each side
     const double *grow;  // GG (rows too large for shared memory): the global row
     bool zrow;           // GG: the current row is all zeros
@@ -118,24 +122,32 @@ struct ClCtx {
 // GG ("global gather"): rows too large for a shared-memory copy next to the
 // Krylov chunks (n = 16384) are gathered straight from L2; publication is
 // then a cluster barrier (release / acquire) instead of a TMA multicast.
-__host__ __device__ inline bool cl_gg(int n) { return n > 8192; }
+// (decided for the largest Krylov space, kMaxKrylovCl + 1 chunk slots)
+constexpr size_t kClSmemMax = 227 * 1024;
+template <int CS>
+__host__ __device__ constexpr bool cl_gg(int n) {
+    return sizeof(ClSmem<CS>) + sizeof(double) * ((size_t)n + 2 * kHalo) +
+               sizeof(double) * (size_t)(kMaxKrylovCl + 1) * (n / CS + 2 * kHalo) > kClSmemMax;
+}
 
+template <int CS>
 __host__ __device__ inline size_t cl_smem_bytes(int n, int K) {
     const int chunk = n / CS;
-    return sizeof(ClSmem) + (cl_gg(n) ? 0 : sizeof(double) * ((size_t)n + 2 * kHalo)) +
+    return sizeof(ClSmem<CS>) + (cl_gg<CS>(n) ? 0 : sizeof(double) * ((size_t)n + 2 * kHalo)) +
            sizeof(double) * (size_t)(K + 1) * (chunk + 2 * kHalo);
 }
 
-__device__ __forceinline__ ClCtx make_clctx(int n, int K, int32_t *status) {
+template <int CS>
+__device__ __forceinline__ ClCtx<CS> make_clctx(int n, int K, int32_t *status) {
     extern __shared__ __align__(128) unsigned char clsm[];
-    ClCtx c;
-    c.S = reinterpret_cast<ClSmem *>(clsm);
-    c.row = reinterpret_cast<double *>(clsm + sizeof(ClSmem)) + kHalo;
+    ClCtx<CS> c;
+    c.S = reinterpret_cast<ClSmem<CS> *>(clsm);
+    c.row = reinterpret_cast<double *>(clsm + sizeof(ClSmem<CS>)) + kHalo;
     c.grow = nullptr;
     c.zrow = false;
     c.chunk = n / CS;
     c.ld = c.chunk + 2 * kHalo;
-    c.slots = cl_gg(n) ? c.row - kHalo : c.row + n + kHalo;
+    c.slots = cl_gg<CS>(n) ? c.row - kHalo : c.row + n + kHalo;
     c.n = n;
     c.rank = ctarank();
     c.base = c.rank * c.chunk;
@@ -158,10 +170,10 @@ struct ArTok {
     uint32_t buf, par;
 };
 
-template <int NPT, int RAD, bool EDGES, bool TWO>
-__device__ __forceinline__ ArTok ar_send(ClCtx &cx, double a, double b, const double (&v)[NPT], int pid = -1) {
+template <int NPT, int RAD, bool EDGES, bool TWO, int CS>
+__device__ __forceinline__ ArTok ar_send(ClCtx<CS> &cx, double a, double b, const double (&v)[NPT], int pid = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    ClSmem &S = *cx.S;
+    ClSmem<CS> &S = *cx.S;
     const ArTok tk{cx.seq & 1, (cx.seq >> 1) & 1};
     ++cx.seq;
     if (pid >= 0) MGRIT_PROBE_AT(pid);
@@ -211,9 +223,9 @@ __device__ __forceinline__ ArTok ar_send(ClCtx &cx, double a, double b, const do
     return tk;
 }
 
-template <bool TWO>
-__device__ __forceinline__ double2 ar_recv(ClCtx &cx, ArTok tk, int pid = -1) {
-    ClSmem &S = *cx.S;
+template <bool TWO, int CS>
+__device__ __forceinline__ double2 ar_recv(ClCtx<CS> &cx, ArTok tk, int pid = -1) {
+    ClSmem<CS> &S = *cx.S;
     mbar_wait(&S.rbar[tk.buf], tk.par);
     if (pid >= 0) MGRIT_PROBE_AT(pid + 3);
     const double *r = S.recv[tk.buf];
@@ -239,12 +251,12 @@ __device__ __forceinline__ double2 ar_recv(ClCtx &cx, ArTok tk, int pid = -1) {
 // plus log2(32/V) butterfly levels), one barrier, warp 0 sums the NWC warp
 // partials and pushes value q to every peer; the receiver sums the CS CTA
 // totals in rank order.
-template <int V, int NV>
-__device__ __forceinline__ double ar_multi(ClCtx &cx, double (&x)[V]) {
+template <int V, int NV, int CS>
+__device__ __forceinline__ double ar_multi(ClCtx<CS> &cx, double (&x)[V]) {
     static_assert(V == 16 || V == 32, "V");
     static_assert(NV <= V, "NV");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    ClSmem &S = *cx.S;
+    ClSmem<CS> &S = *cx.S;
     const uint32_t buf = cx.seq & 1, par = (cx.seq >> 1) & 1;
     ++cx.seq;
 #pragma unroll
@@ -295,8 +307,8 @@ __device__ __forceinline__ double ar_multi(ClCtx &cx, double (&x)[V]) {
 // that an earlier kernel wrote) into the full-row buffer of all CTAs; rank 0
 // and rank CS-1 also supply the periodic halos.  GG: the chunk stores are
 // released with a cluster-barrier arrive; await_row is the acquire wait.
-template <bool GG>
-__device__ __forceinline__ void publish_row(ClCtx &cx, const double *src) {
+template <bool GG, int CS>
+__device__ __forceinline__ void publish_row(ClCtx<CS> &cx, const double *src) {
     if constexpr (GG) {
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         cx.grow = src;
@@ -306,7 +318,7 @@ __device__ __forceinline__ void publish_row(ClCtx &cx, const double *src) {
     fence_async_global();
     __syncthreads();
     if (threadIdx.x == 0) {
-        ClSmem &S = *cx.S;
+        ClSmem<CS> &S = *cx.S;
         const uint32_t bar = su32(&S.rowbar);
         const uint16_t mask = (uint16_t)((1u << CS) - 1);
         mbar_expect_tx(&S.rowbar, (uint32_t)((cx.n + 2 * kHalo) * 8));
@@ -315,8 +327,8 @@ __device__ __forceinline__ void publish_row(ClCtx &cx, const double *src) {
         if (cx.rank == CS - 1) bulk_multicast(su32(cx.row - kHalo), src + cx.n - kHalo, kHalo * 8, bar, mask);
     }
 }
-template <bool GG>
-__device__ __forceinline__ void await_row(ClCtx &cx) {
+template <bool GG, int CS>
+__device__ __forceinline__ void await_row(ClCtx<CS> &cx) {
     if constexpr (GG) {
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         return;
@@ -325,8 +337,8 @@ __device__ __forceinline__ void await_row(ClCtx &cx) {
     ++cx.pubs;
 }
 // local all-zero row (no publication)
-template <bool GG>
-__device__ __forceinline__ void zero_row(ClCtx &cx) {
+template <bool GG, int CS>
+__device__ __forceinline__ void zero_row(ClCtx<CS> &cx) {
     if constexpr (GG) {
         cx.zrow = true;
         return;
@@ -336,23 +348,23 @@ __device__ __forceinline__ void zero_row(ClCtx &cx) {
     __syncthreads();
 }
 
-template <int NPT>
-__device__ __forceinline__ void load_chunk(const ClCtx &cx, double (&v)[NPT], const double *src) {
+template <int NPT, int CS>
+__device__ __forceinline__ void load_chunk(const ClCtx<CS> &cx, double (&v)[NPT], const double *src) {
 #pragma unroll
     for (int k = 0; k < NPT; ++k) v[k] = src[cx.base + threadIdx.x + k * NTC];
 }
-template <int NPT>
-__device__ __forceinline__ void store_chunk(const ClCtx &cx, double *dst, const double (&v)[NPT]) {
+template <int NPT, int CS>
+__device__ __forceinline__ void store_chunk(const ClCtx<CS> &cx, double *dst, const double (&v)[NPT]) {
 #pragma unroll
     for (int k = 0; k < NPT; ++k) dst[cx.base + threadIdx.x + k * NTC] = v[k];
 }
-template <int NPT>
-__device__ __forceinline__ void add_forcing_chunk(const ClCtx &cx, double (&v)[NPT], const double *g) {
+template <int NPT, int CS>
+__device__ __forceinline__ void add_forcing_chunk(const ClCtx<CS> &cx, double (&v)[NPT], const double *g) {
 #pragma unroll
     for (int k = 0; k < NPT; ++k) v[k] = __dadd_rn(v[k], g ? g[cx.base + threadIdx.x + k * NTC] : 0.0);
 }
-template <int NPT>
-__device__ __forceinline__ void load_records_chunk(const ClCtx &cx, const mgrit_level_desc &L, int64_t t,
+template <int NPT, int CS>
+__device__ __forceinline__ void load_records_chunk(const ClCtx<CS> &cx, const mgrit_level_desc &L, int64_t t,
                                                    double (&sv)[NPT]) {
     const double *s = L.s_x + (L.shared ? 0 : t) * (int64_t)cx.n + cx.base;
 #pragma unroll
@@ -364,19 +376,18 @@ __device__ __forceinline__ void load_records_chunk(const ClCtx &cx, const mgrit_
 // GmresConfig.max_iters); every thread keeps the Givens rotations in
 // registers and evaluates them redundantly (identical inputs -> identical
 // results in every thread and CTA), so the stop test needs no barrier.
-constexpr int kMaxKrylovCl = 10;
 
 // v (chunk) = Phi_t(row): SL gather from the full row, then GMRES on
 // (I - diag(sig) D) x = v with the cluster reductions above.  Returns the
 // Arnoldi count (-1 on a non-finite right-hand side).
-template <int P, int NPT, bool NUMBA, bool LOWSYNC, bool GG>
-__device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double (&v)[NPT],
+template <int P, int NPT, bool NUMBA, bool LOWSYNC, bool GG, int CS>
+__device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx<CS> &cx, double (&v)[NPT],
                         const double (&sv)[NPT], bool wait_row) {
     constexpr int SLW = Stencil<P>::L;
     constexpr int RAD = (P + 1) / 2;
     constexpr int KM = kMaxKrylovCl;
     const int n = cx.n, tid = threadIdx.x;
-    ClSmem &S = *cx.S;
+    ClSmem<CS> &S = *cx.S;
     // ---- semi-Lagrangian gather (same arithmetic as cta_apply)
     MGRIT_PROBE_AT(400);
     if (wait_row) await_row<GG>(cx);
@@ -658,7 +669,8 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx &cx, double 
     return done;
 }
 
-__device__ __forceinline__ void cl_init(ClCtx &cx) {
+template <int CS>
+__device__ __forceinline__ void cl_init(ClCtx<CS> &cx) {
     if (threadIdx.x == 0) {
         mbar_init(&cx.S->rbar[0], 1);
         mbar_init(&cx.S->rbar[1], 1);
@@ -671,11 +683,11 @@ __device__ __forceinline__ void cl_init(ClCtx &cx) {
 // --------------------------------------------------------- level phases --
 // Same phase semantics as phase_kernel (mgrit_b200.h MGRIT_PHASE_*), one
 // cluster per C-interval (persistent over intervals).
-template <int P, int NPT, bool LOWSYNC, bool GG>
+template <int P, int NPT, bool LOWSYNC, bool GG, int CS>
 __global__ void __launch_bounds__(NTC) cl_phase_kernel(mgrit_level_desc L, mgrit_phase_args A, int32_t *status) {
     const int n = L.n_x;
     const int m = A.m;
-    ClCtx cx = make_clctx(n, L.gmres_max_iters, status);
+    ClCtx<CS> cx = make_clctx<CS>(n, L.gmres_max_iters, status);
     cl_init(cx);
     auto U = [&](int64_t t) { return A.U + (t - A.u_row0) * A.ldu; };
     auto Gr = [&](int64_t t) -> const double * { return A.G ? A.G + (t - A.g_row0) * A.ldg : nullptr; };
@@ -729,7 +741,7 @@ __global__ void __launch_bounds__(NTC) cl_phase_kernel(mgrit_level_desc L, mgrit
 #pragma unroll 1
         for (int k = 1; k <= kmax; ++k) {
             const int64_t t = t0 + k;
-            cl_apply<P, NPT, false, LOWSYNC, GG>(L, t - 1, cx, v, sv, have_pub);
+            cl_apply<P, NPT, false, LOWSYNC, GG, CS>(L, t - 1, cx, v, sv, have_pub);
             have_pub = true;
             if (k < kmax) load_records_chunk<NPT>(cx, L, t, sv);
             if (k < m) {
@@ -785,12 +797,12 @@ __global__ void __launch_bounds__(NTC) cl_phase_kernel(mgrit_level_desc L, mgrit
 }
 
 // ------------------------------------------------------ sequential sweep --
-template <int P, int NPT, bool NUMBA, bool LOWSYNC, bool GG>
+template <int P, int NPT, bool NUMBA, bool LOWSYNC, bool GG, int CS>
 __global__ void __launch_bounds__(NTC) cl_sweep_kernel(mgrit_level_desc L, double *U, int64_t ldu, const double *G,
                                                        int64_t ldg, int zero_init, int32_t *gmres_iters,
                                                        int32_t *status) {
     const int n = L.n_x;
-    ClCtx cx = make_clctx(n, L.gmres_max_iters, status);
+    ClCtx<CS> cx = make_clctx<CS>(n, L.gmres_max_iters, status);
     cl_init(cx);
     double v[NPT], sv[NPT];
     load_records_chunk<NPT>(cx, L, 0, sv);
@@ -805,7 +817,7 @@ __global__ void __launch_bounds__(NTC) cl_sweep_kernel(mgrit_level_desc L, doubl
     }
 #pragma unroll 1
     for (int64_t t = 0; t < L.n_steps; ++t) {
-        const int cnt = cl_apply<P, NPT, NUMBA, LOWSYNC, GG>(L, t, cx, v, sv, have_pub);
+        const int cnt = cl_apply<P, NPT, NUMBA, LOWSYNC, GG, CS>(L, t, cx, v, sv, have_pub);
         have_pub = true;
         if (t + 1 < L.n_steps) load_records_chunk<NPT>(cx, L, t + 1, sv);
         add_forcing_chunk<NPT>(cx, v, G ? G + (t + 1) * ldg : nullptr);
@@ -817,22 +829,31 @@ __global__ void __launch_bounds__(NTC) cl_sweep_kernel(mgrit_level_desc L, doubl
 }
 
 // ------------------------------------------------------------- launchers --
-// Eligible: corrected 1D level, n in {1024, 2048, 4096, 8192}, every row
-// pointer / leading dimension 16-byte aligned (TMA bulk copies).
+// Eligible: corrected 1D level whose row splits into CS chunks of 128 x NP
+// nodes (NP in {1, 2, 4, 8, 16}) with the Krylov chunk slots in shared
+// memory; every row pointer / leading dimension 16-byte aligned (TMA bulk
+// copies).
 inline bool cl_aligned(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
+template <int CS>
+inline int cl_npt(int n) {
+    if (n % (CS * NTC)) return 0;
+    const int np = n / (CS * NTC);
+    return (np == 1 || np == 2 || np == 4 || np == 8 || np == 16) ? np : 0;
+}
+
+template <int CS>
 inline bool cl_eligible(const mgrit_level_desc *L) {
     if (L->kind != MGRIT_KIND_CORRECTED || L->dim != 1) return false;
-    const int n = L->n_x;
-    if (n != 1024 && n != 2048 && n != 4096 && n != 8192 && n != 16384) return false;
-    // (n = 16384: 16 nodes per thread leave no registers for the low-sync
-    //  variant; those launches run classic MGS, see LaunchCl)
+    if (!cl_npt<CS>(L->n_x)) return false;
+    // (16 nodes per thread leave no registers for the low-sync variant;
+    //  those launches run classic MGS, see LaunchCl)
     if (L->gmres_max_iters < 1 || L->gmres_max_iters > kMaxKrylovCl) return false;
-    if (cl_smem_bytes(n, L->gmres_max_iters) > (size_t)max_smem_optin()) return false;
+    if (cl_smem_bytes<CS>(L->n_x, L->gmres_max_iters) > (size_t)max_smem_optin()) return false;
     return true;
 }
 
-template <int P>
+template <int P, int CS>
 struct LaunchCl {
     static int phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int32_t *status, cudaStream_t st,
                      int max_clusters);
@@ -842,18 +863,19 @@ struct LaunchCl {
 };
 
 #ifdef MGRIT_LAUNCHCL_IMPL
-template <typename Fn>
+template <int CS, typename Fn>
 static int cl_dispatch_npt(int n, Fn &&f) {
-    switch (n) {
-        case 1024: return f(std::integral_constant<int, 1>{});
-        case 2048: return f(std::integral_constant<int, 2>{});
-        case 4096: return f(std::integral_constant<int, 4>{});
-        case 8192: return f(std::integral_constant<int, 8>{});
-        default: return f(std::integral_constant<int, 16>{});
+    switch (cl_npt<CS>(n)) {
+        case 1: return f(std::integral_constant<int, 1>{});
+        case 2: return f(std::integral_constant<int, 2>{});
+        case 4: return f(std::integral_constant<int, 4>{});
+        case 8: return f(std::integral_constant<int, 8>{});
+        case 16: return f(std::integral_constant<int, 16>{});
+        default: set_error("cluster launch: unsupported row length", cudaErrorInvalidValue); return (int)MGRIT_EINVAL;
     }
 }
 
-template <typename K>
+template <int CS, typename K>
 static cudaLaunchConfig_t cl_config(K, int grid, size_t smem, cudaStream_t st, cudaLaunchAttribute *attr) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
@@ -869,9 +891,11 @@ static cudaLaunchConfig_t cl_config(K, int grid, size_t smem, cudaStream_t st, c
     return cfg;
 }
 
-template <typename Fn>
+template <int CS, typename Fn>
 static int cl_prep(Fn fn, size_t smem) {
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && CS > 8)
+        e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute(cluster)", e);
         return MGRIT_ECUDA;
@@ -879,15 +903,19 @@ static int cl_prep(Fn fn, size_t smem) {
     return MGRIT_OK;
 }
 
-template <int P>
-int LaunchCl<P>::resident_clusters(const mgrit_level_desc *L) {
-    const size_t smem = cl_smem_bytes(L->n_x, L->gmres_max_iters);
-    return cl_dispatch_npt(L->n_x, [&](auto N) {
+// GG for the row length that NP nodes per thread imply
+template <int CS, int NP>
+constexpr bool cl_gg_np() { return cl_gg<CS>(NP * CS * NTC); }
+
+template <int P, int CS>
+int LaunchCl<P, CS>::resident_clusters(const mgrit_level_desc *L) {
+    const size_t smem = cl_smem_bytes<CS>(L->n_x, L->gmres_max_iters);
+    const int r = cl_dispatch_npt<CS>(L->n_x, [&](auto N) {
         constexpr int NP = decltype(N)::value;
-        auto fn = cl_phase_kernel<P, NP, false, (NP > 8)>;
-        if (cl_prep(fn, smem)) return 0;
+        auto fn = cl_phase_kernel<P, NP, false, cl_gg_np<CS, NP>(), CS>;
+        if (cl_prep<CS>(fn, smem)) return 0;
         cudaLaunchAttribute attr[1];
-        cudaLaunchConfig_t cfg = cl_config(fn, CS, smem, 0, attr);
+        cudaLaunchConfig_t cfg = cl_config<CS>(fn, CS, smem, 0, attr);
         int ncl = 0;
         if (cudaOccupancyMaxActiveClusters(&ncl, (void *)fn, &cfg) != cudaSuccess) {
             cudaGetLastError();
@@ -895,20 +923,21 @@ int LaunchCl<P>::resident_clusters(const mgrit_level_desc *L) {
         }
         return ncl;
     });
+    return r < 0 ? 0 : r;
 }
 
-template <int P>
-int LaunchCl<P>::phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int32_t *status, cudaStream_t st,
-                       int max_clusters) {
-    const size_t smem = cl_smem_bytes(L->n_x, L->gmres_max_iters);
-    const int rc = cl_dispatch_npt(L->n_x, [&](auto N) {
+template <int P, int CS>
+int LaunchCl<P, CS>::phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int32_t *status, cudaStream_t st,
+                           int max_clusters) {
+    const size_t smem = cl_smem_bytes<CS>(L->n_x, L->gmres_max_iters);
+    const int rc = cl_dispatch_npt<CS>(L->n_x, [&](auto N) {
         auto launch = [&](auto fn) {
-            int r = cl_prep(fn, smem);
+            int r = cl_prep<CS>(fn, smem);
             if (r) return r;
             int64_t ncl = A->c_count < max_clusters ? A->c_count : max_clusters;
             if (ncl < 1) ncl = 1;
             cudaLaunchAttribute attr[1];
-            cudaLaunchConfig_t cfg = cl_config(fn, (int)(ncl * CS), smem, st, attr);
+            cudaLaunchConfig_t cfg = cl_config<CS>(fn, (int)(ncl * CS), smem, st, attr);
             cudaError_t e = cudaLaunchKernelEx(&cfg, fn, *L, *A, status);
             if (e != cudaSuccess) {
                 set_error("cudaLaunchKernelEx(cl_phase)", e);
@@ -917,26 +946,26 @@ int LaunchCl<P>::phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int
             return (int)MGRIT_OK;
         };
         constexpr int NP = decltype(N)::value;
-        if constexpr (NP <= 8) {
-            if (L->gmres_lowsync) return launch(cl_phase_kernel<P, NP, true, false>);
+        if constexpr (NP <= 8 && !cl_gg_np<CS, NP>()) {
+            if (L->gmres_lowsync) return launch(cl_phase_kernel<P, NP, true, false, CS>);
         }
-        return launch(cl_phase_kernel<P, NP, false, (NP > 8)>);
+        return launch(cl_phase_kernel<P, NP, false, cl_gg_np<CS, NP>(), CS>);
     });
     if (rc) return rc;
     return check_launch("level_phase(cluster)");
 }
 
-template <int P>
-int LaunchCl<P>::sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg,
-                       int zero_init, int32_t *gmres_iters, int32_t *status, cudaStream_t st) {
-    const size_t smem = cl_smem_bytes(L->n_x, L->gmres_max_iters);
+template <int P, int CS>
+int LaunchCl<P, CS>::sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg,
+                           int zero_init, int32_t *gmres_iters, int32_t *status, cudaStream_t st) {
+    const size_t smem = cl_smem_bytes<CS>(L->n_x, L->gmres_max_iters);
     const bool numba = L->stencil_numba != 0;
-    const int rc = cl_dispatch_npt(L->n_x, [&](auto N) {
+    const int rc = cl_dispatch_npt<CS>(L->n_x, [&](auto N) {
         auto launch = [&](auto fn) {
-            int r = cl_prep(fn, smem);
+            int r = cl_prep<CS>(fn, smem);
             if (r) return r;
             cudaLaunchAttribute attr[1];
-            cudaLaunchConfig_t cfg = cl_config(fn, CS, smem, st, attr);
+            cudaLaunchConfig_t cfg = cl_config<CS>(fn, CS, smem, st, attr);
             cudaError_t e = cudaLaunchKernelEx(&cfg, fn, *L, U, ldu, G, ldg, zero_init, gmres_iters, status);
             if (e != cudaSuccess) {
                 set_error("cudaLaunchKernelEx(cl_sweep)", e);
@@ -945,15 +974,15 @@ int LaunchCl<P>::sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const 
             return (int)MGRIT_OK;
         };
         constexpr int NP = decltype(N)::value;
-        constexpr bool GG = NP > 8;
-        if constexpr (NP <= 8) {
+        constexpr bool GG = cl_gg_np<CS, NP>();
+        if constexpr (NP <= 8 && !GG) {
             if (L->gmres_lowsync) {
-                if (numba) return launch(cl_sweep_kernel<P, NP, true, true, false>);
-                return launch(cl_sweep_kernel<P, NP, false, true, false>);
+                if (numba) return launch(cl_sweep_kernel<P, NP, true, true, false, CS>);
+                return launch(cl_sweep_kernel<P, NP, false, true, false, CS>);
             }
         }
-        if (numba) return launch(cl_sweep_kernel<P, NP, true, false, GG>);
-        return launch(cl_sweep_kernel<P, NP, false, false, GG>);
+        if (numba) return launch(cl_sweep_kernel<P, NP, true, false, GG, CS>);
+        return launch(cl_sweep_kernel<P, NP, false, false, GG, CS>);
     });
     if (rc) return rc;
     return check_launch("sequential_sweep(cluster)");

@@ -852,7 +852,7 @@ inline int cap_grid(int64_t want, int resident, const mgrit_level_desc *L, int64
 // parallel.
 template <int P, int KIND>
 struct Launch1D {
-    static int64_t capacity(const mgrit_level_desc *L);
+    static int64_t capacity(const mgrit_level_desc *L, bool one_per_sm);
     static int rows(const mgrit_level_desc *L, const RowsArgs &a, void *scratch,
                     int64_t scratch_bytes, int32_t *status, cudaStream_t st);
     static int phase(const mgrit_level_desc *L, const mgrit_phase_args *A, void *scratch,
@@ -864,7 +864,7 @@ struct Launch1D {
 
 #ifdef MGRIT_LAUNCH1D_IMPL
 template <int P, int KIND>
-int64_t Launch1D<P, KIND>::capacity(const mgrit_level_desc *L) {
+int64_t Launch1D<P, KIND>::capacity(const mgrit_level_desc *L, bool one_per_sm) {
     const Cfg1D c = cfg_for(L->n_x);
     const int nbs = smem_slots(L);
     const size_t smem = smem_bytes_for(L->n_x, nbs);
@@ -874,6 +874,7 @@ int64_t Launch1D<P, KIND>::capacity(const mgrit_level_desc *L) {
         if (prep(fn, smem)) return 1;
         int cap = resident_ctas((const void *)fn, C::NT, smem);
         if constexpr (TwoPerSM<C>::value) {
+            if (one_per_sm) return cap;
             // the phase kernel's two-CTAs-per-SM form (scratch is sized from this)
             const size_t smem2 = smem_bytes_for(L->n_x, smem_slots_two(L));
             auto fn2 = phase_kernel<C::P, C::KIND, C::NT, C::NPT, C::F, 2>;

@@ -36,15 +36,19 @@ _KIND_CODE = {"fine": _lib.KIND_SL, "rediscretized": _lib.KIND_SL, "corrected": 
 
 
 GMRES_VARIANTS = ("mgs", "mgs_lowsync")
-LAUNCH_POLICIES = {"auto": 0, "cta": 1, "cluster": 2, "auto_one": 3}
+LAUNCH_POLICIES = {"auto": 0, "cta": 1, "cluster": 2, "auto_one": 3,
+                   "cluster2": 4, "cluster4": 5, "cluster8": 6, "cluster16": 7}
 _launch_policy = "auto"
 
 
 def set_launch_policy(policy: str) -> str:
-    """Kernel shape of corrected 1D phases/sweeps: "auto" (cluster-split when a
-    level has too few row chains to fill the GPU), "cta" (one CTA per row
-    chain) or "cluster" (8-CTA cluster per row chain whenever eligible).
-    Returns the previous policy."""
+    """Kernel shape of corrected 1D phases/sweeps: "auto" (per level, the
+    shape with the lowest measured cost: one CTA per row chain, two per SM
+    when chains outnumber SMs, or a 2/4/8/16-CTA cluster per chain when a
+    level has too few chains to fill the GPU), "auto_one" (auto without the
+    two-per-SM form), "cta" (CTA kernels only), "cluster" (a cluster per
+    chain whenever eligible, size by cost) or "cluster2/4/8/16" (that
+    cluster size wherever eligible).  Returns the previous policy."""
     global _launch_policy
     if policy not in LAUNCH_POLICIES:
         raise ValueError(f"launch policy must be one of {sorted(LAUNCH_POLICIES)}")

@@ -598,14 +598,34 @@ def test_cfg2_full_size_cluster_matches_reference(P, golden_index, cluster_polic
     assert np.allclose(np.linalg.norm(U, axis=1), g["row_norms"], rtol=1e-12, atol=0)
 
 
-@pytest.mark.parametrize("variant", ["mgs", "mgs_lowsync"])
+@pytest.mark.parametrize("size,variant", [(8, "mgs"), (8, "mgs_lowsync"), (2, "mgs"), (4, "mgs"),
+                                          (4, "mgs_lowsync"), (16, "mgs")])
 @pytest.mark.parametrize("n_x,p,speed,m,levels", [(1024, 1, "C1", 4, None), (2048, 3, "C3", 4, None),
                                                   (4096, 5, "B2", 8, None), (8192, 3, "C2", 4, 2),
                                                   (2048, 5, "C3", 16, 2)])
-def test_cluster_solve_matches_oracle(P, cluster_policy, n_x, p, speed, m, levels, variant):
-    """Every cluster configuration (n = 1024 .. 8192, p = 1/3/5, two-level
-    fixed-K and multilevel tolerance GMRES) against the oracle."""
-    kw = dict(n_x=n_x, n_t=64, wave_speed=speed, p=p, schedule=m, max_levels=levels, seed=3,
+def test_cluster_solve_matches_oracle(P, n_x, p, speed, m, levels, size, variant):
+    """Every cluster configuration (2/4/8/16 CTAs per cluster where the row
+    splits into 128 x {1,2,4,8,16}-node chunks, n = 1024 .. 8192, p = 1/3/5,
+    two-level fixed-K and multilevel tolerance GMRES) against the oracle."""
+    prev = P.set_launch_policy(f"cluster{size}")
+    try:
+        _cluster_solve_vs_oracle(P, n_x, p, speed, m, levels, variant)
+    finally:
+        P.set_launch_policy(prev)
+
+
+@pytest.mark.parametrize("size", [8, 16])
+def test_cluster_n16384_matches_oracle(P, size):
+    """Config 3's row length on 8- and 16-CTA clusters (global-gather rows)."""
+    prev = P.set_launch_policy(f"cluster{size}")
+    try:
+        _cluster_solve_vs_oracle(P, 16384, 5, "B2", 8, None, "mgs", n_t=128)
+    finally:
+        P.set_launch_policy(prev)
+
+
+def _cluster_solve_vs_oracle(P, n_x, p, speed, m, levels, variant, n_t=64):
+    kw = dict(n_x=n_x, n_t=n_t, wave_speed=speed, p=p, schedule=m, max_levels=levels, seed=3,
               max_iters=5, rtol=0.0)
     cfg, ocfg = _cfg_pair(P, kw)
     cfg = P.SolverConfig(**kw, gmres_variant=variant)

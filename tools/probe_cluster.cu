@@ -42,7 +42,7 @@ int main(int argc, char **argv) {
     L.s_x = ds; L.sig_x = dsig; L.gmres_max_iters = K; L.gmres_tol = -1.0; L.gmres_lowsync = lowsync;
     for (int rep = 0; rep < 3; ++rep) {
         cudaMemcpy(du, u.data(), (steps + 1) * n * 8, cudaMemcpyHostToDevice);
-        int rc = cl::LaunchCl<3>::sweep(&L, du, n, nullptr, 0, 0, nullptr, st, 0);
+        int rc = cl::LaunchCl<3, 8>::sweep(&L, du, n, nullptr, 0, 0, nullptr, st, 0);
         if (rc) { printf("launch rc %d\n", rc); return 1; }
     }
     cudaError_t e = cudaDeviceSynchronize();
