@@ -706,7 +706,7 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
     state = "max_iters"
     G0 = torch.zeros_like(U) if not use_fused else None
 
-    if use_fused and use_graph:
+    if use_fused and use_graph and cfg.max_iters >= 1:
         # device-resident loop: one graph launch, one host sync per solve
         loop = _solve_loop(sess, cfg, status)
         lib = _lib.load()
@@ -793,7 +793,10 @@ class _Loop:
 
     def __del__(self):
         if self.handle:
-            _lib.load().mgrit_loop_destroy(self.handle)
+            try:
+                _lib.load().mgrit_loop_destroy(self.handle)
+            except Exception:  # interpreter shutdown: the library may be gone
+                pass
             self.handle = None
 
 

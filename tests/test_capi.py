@@ -35,6 +35,22 @@ def test_header_symbols_exported():
         assert re.search(rf"\bT {n}\b", out), n
 
 
+def test_loop_entry_points_reject_bad_arguments():
+    """The device-loop entry points validate their arguments before touching
+    CUDA (no device needed): the legacy stream cannot be captured, NULL
+    handles and buffers are rejected."""
+    from paper_2203_13382_b200 import _lib
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    assert lib.mgrit_loop_begin(None, ctypes.byref(h)) == _lib.MGRIT_EINVAL
+    assert lib.mgrit_loop_check(None, 8, 8, 8, 8, 8, None) == _lib.MGRIT_EINVAL
+    assert lib.mgrit_loop_end(None, None) == _lib.MGRIT_EINVAL
+    assert lib.mgrit_loop_launch(None, None) == _lib.MGRIT_EINVAL
+    assert lib.mgrit_loop_init(None, 8, 8, 8, 1e-10, 1e6, 10, None) == _lib.MGRIT_EINVAL
+    assert lib.mgrit_loop_init(8, 8, 8, 8, 1e-10, 1e6, 0, None) == _lib.MGRIT_EINVAL
+    lib.mgrit_loop_destroy(None)
+
+
 def test_library_is_sm100a():
     from paper_2203_13382_b200 import _lib
     r = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)

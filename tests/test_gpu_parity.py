@@ -373,6 +373,43 @@ def test_graph_replay_equals_eager(P):
     assert np.array_equal(r1.residual_norms, r2.residual_norms)
 
 
+@pytest.mark.parametrize("kw", [dict(max_iters=4, rtol=0.0), dict(max_iters=50, rtol=1e-10),
+                                dict(max_iters=3, rtol=1e-10)])
+def test_device_loop_stop_rule_matches_host_loop(P, kw):
+    """The device-resident loop (CUDA-graph WHILE node) stops exactly where the
+    reference's host loop does: max_iters, converged, and max_iters reached
+    before convergence; same histories bit for bit."""
+    cfg = P.SolverConfig(n_x=128, n_t=256, wave_speed="B2", p=3, schedule=4, **kw)
+    levels = P.build_hierarchy(cfg)
+    r1, U1 = P.solve(cfg, levels, use_graph=True)
+    r2, U2 = P.solve(cfg, levels, use_graph=False)
+    assert r1.status == r2.status and r1.iterations == r2.iterations
+    assert np.array_equal(r1.residual_norms, r2.residual_norms)
+    assert np.array_equal(U1, U2)
+    assert r1.status == ("max_iters" if kw["rtol"] == 0.0 or kw["max_iters"] == 3 else "converged")
+
+
+def test_device_loop_non_finite_iterate_diverges_like_reference(P):
+    """A NaN in the initial iterate at a C-point (U[40], m = 4) survives
+    F-relaxation, reaches a coarse GMRES right-hand side, and the reference
+    turns that into ValueError -> status "diverged" with a NaN history entry
+    (mgrit.py:363-366).  A NaN at an F-point is overwritten by the first
+    F-relaxation; r0 is NaN, so the stop rule never fires and the reference
+    runs to max_iters.  Both outcomes are reproduced."""
+    kw = dict(n_x=128, n_t=256, wave_speed="B2", p=3, schedule=4, max_iters=12)
+    cfg, ocfg = _cfg_pair(P, kw)
+    for row, want in ((39, "diverged"), (37, "max_iters")):
+        it0 = O.initial_iterate(ocfg)
+        it0[row, 5] = np.nan
+        orep, _ = O.solve(ocfg, iterate0=it0)
+        assert orep.status == want
+        for use_graph in (True, False):
+            rep, _ = P.solve(cfg, initial_iterate=it0, use_graph=use_graph)
+            assert rep.status == orep.status
+            assert rep.iterations == orep.iterations
+            assert np.array_equal(np.isnan(rep.residual_norms), np.isnan(orep.residual_norms))
+
+
 def test_sequential_reference_matches_oracle(P):
     kw = dict(n_x=128, n_t=256, wave_speed="B2", p=5, schedule=4)
     cfg, ocfg = _cfg_pair(P, kw)
