@@ -144,21 +144,36 @@ class SolverConfig:
 
 
 class _Workspace:
+    """Per-device scratch and sticky status flag.  The status tensor of a
+    device is never reallocated: captured graphs (the solve loop) keep its
+    address."""
+
     def __init__(self):
-        self.scratch: torch.Tensor | None = None
-        self.status: torch.Tensor | None = None
+        self.scratch: dict = {}
+        self.status: dict = {}
+
+    @staticmethod
+    def _key(device) -> torch.device:
+        d = torch.device(device)
+        return torch.device(d.type, torch.cuda.current_device()) if d.type == "cuda" and d.index is None else d
 
     def get_scratch(self, nbytes: int, device) -> torch.Tensor:
         if nbytes <= 0:
             return None
-        if self.scratch is None or self.scratch.numel() < nbytes or self.scratch.device != device:
-            self.scratch = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
-        return self.scratch
+        key = self._key(device)
+        buf = self.scratch.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(int(nbytes), dtype=torch.uint8, device=key)
+            self.scratch[key] = buf
+        return buf
 
     def get_status(self, device) -> torch.Tensor:
-        if self.status is None or self.status.device != device:
-            self.status = torch.zeros(1, dtype=torch.int32, device=device)
-        return self.status
+        key = self._key(device)
+        st = self.status.get(key)
+        if st is None:
+            st = torch.zeros(1, dtype=torch.int32, device=key)
+            self.status[key] = st
+        return st
 
 
 _WS = _Workspace()
