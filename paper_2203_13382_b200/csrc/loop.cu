@@ -88,8 +88,10 @@ extern "C" int mgrit_loop_begin(void *stream, void **loop_out) {
     if (e == cudaSuccess) {
         lp->body = p.conditional.phGraph_out[0];
         lp->capture = (cudaStream_t)stream;
+        // relaxed: API calls the host code makes meanwhile (attribute and
+        // occupancy queries, frees) cannot invalidate the capture
         e = cudaStreamBeginCaptureToGraph(lp->capture, lp->body, nullptr, nullptr, 0,
-                                          cudaStreamCaptureModeThreadLocal);
+                                          cudaStreamCaptureModeRelaxed);
     }
     if (e != cudaSuccess) {
         if (lp->graph) cudaGraphDestroy(lp->graph);
@@ -140,9 +142,14 @@ extern "C" void mgrit_loop_destroy(void *loop) {
     Loop *lp = (Loop *)loop;
     if (!lp) return;
     if (lp->capture) {
+        // abandon an unfinished capture; the half-built graph is leaked on
+        // purpose (destroying a graph whose conditional body capture was
+        // invalidated is not safe on every driver)
         cudaGraph_t g = nullptr;
-        cudaStreamEndCapture(lp->capture, &g);  // abandon an unfinished capture
+        cudaStreamEndCapture(lp->capture, &g);
         cudaGetLastError();
+        delete lp;
+        return;
     }
     if (lp->exec) cudaGraphExecDestroy(lp->exec);
     if (lp->graph) cudaGraphDestroy(lp->graph);

@@ -496,6 +496,29 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx<CS> &cx, dou
     double g_k = beta;
     double gmax = 0.0;      // warp 0: max |<b_i, b_j>|, i != j (low-sync)
     int done = 0;
+    // The rotation of column kk (and the stop test it feeds) is applied after
+    // the NEXT Arnoldi step's stencil: the two are independent, so the
+    // rotation's dependent chain (hypot, reciprocal, divisions) overlaps the
+    // stencil instead of following it.  If the test stops the iteration, that
+    // stencil's result is discarded (it only wrote registers), so the
+    // arithmetic and the step count are those of the reference's loop.
+    double hprev = 0.0, nprev = 0.0;  // column kk-1: rotated H[kk-1][kk-1], h_{kk,kk-1}
+    bool bprev = false, stopped = false;
+    auto rotation = [&](int col, double hr, double nr, double &c_out, double &s_out) {
+        const double den = hypot(hr, nr);
+        const double rden = __drcp_rn(den);
+        c_out = div_rcp(hr, den, rden);
+        s_out = div_rcp(nr, den, rden);
+        const double gn = __dmul_rn(-s_out, g_k);
+        if (tid == 0) {
+            S.H[col * kMaxKrylov + col] = den;
+            S.rdiag[col] = rden;
+            S.g[col] = __dmul_rn(c_out, g_k);
+        }
+        g_k = gn;
+        done = col + 1;
+        return fabs(gn) <= __dmul_rn(tol, beta);
+    };
 #pragma unroll
     for (int kk = 0; kk < KM; ++kk) {
         if (kk >= K) break;
@@ -504,6 +527,13 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx<CS> &cx, dou
         const double *bk = cx.slot(kk);
 #pragma unroll
         for (int k = 0; k < NPT; ++k) v[k] = imsd_at(bk, k, tid + k * NTC, v[k]);
+        if (kk > 0) {
+            const bool conv = rotation(kk - 1, hprev, nprev, cs[kk - 1], sn[kk - 1]);
+            if (bprev || (tol >= 0.0 && conv)) {
+                stopped = true;
+                break;
+            }
+        }
         MGRIT_PROBE_AT(411 + 6 * kk);
         double h[KM];
         if constexpr (LOWSYNC) {
@@ -613,21 +643,15 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx<CS> &cx, dou
             put_slot(kk + 1, nrm, yn, tn.buf);
         }
         MGRIT_PROBE_AT(414 + 6 * kk);
-        // new rotation from (H[kk][kk], h_{kk+1,kk} = nrm), every thread
-        const double den = hypot(hrun, nrm);
-        const double rden = __drcp_rn(den);
-        cs[kk] = div_rcp(hrun, den, rden);
-        sn[kk] = div_rcp(nrm, den, rden);
-        const double gn = __dmul_rn(-sn[kk], g_k);
-        if (tid == 0) {
-            S.H[kk * kMaxKrylov + kk] = den;
-            S.rdiag[kk] = rden;
-            S.g[kk] = __dmul_rn(cs[kk], g_k);
-        }
-        g_k = gn;
-        done = kk + 1;
+        hprev = hrun;
+        nprev = nrm;
+        bprev = brk;
         MGRIT_PROBE_AT(415 + 6 * kk);
-        if (brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta))) break;
+    }
+    if (!stopped) {
+        // the last column's rotation (the iteration ended at K steps)
+        double c_last, s_last;
+        rotation(K - 1, hprev, nprev, c_last, s_last);
     }
     __syncthreads();  // S.H / S.g / S.rdiag from thread 0
     MGRIT_PROBE_AT(482);

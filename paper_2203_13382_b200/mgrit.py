@@ -17,6 +17,7 @@ what the drop-in functions compose; both paths give identical iterates.
 from __future__ import annotations
 
 import ctypes
+import gc
 import time
 from dataclasses import dataclass, field, replace
 from typing import Sequence
@@ -799,6 +800,18 @@ class _Session:
     loop: "_Loop | None" = None
 
 
+# Loops whose owner was garbage-collected.  They are destroyed only at a safe
+# point (_flush_loops, outside any stream capture): the cyclic GC can run a
+# finaliser while another loop is being captured, and destroying a graph
+# during a capture invalidates that capture.
+_DEAD_LOOPS: list = []
+
+
+def _flush_loops():
+    while _DEAD_LOOPS:
+        _lib.load().mgrit_loop_destroy(_DEAD_LOOPS.pop())
+
+
 class _Loop:
     """The captured device-resident convergence loop (loop.cu): a CUDA graph
     whose WHILE node runs one V-cycle + the stop test per pass."""
@@ -808,10 +821,7 @@ class _Loop:
 
     def __del__(self):
         if self.handle:
-            try:
-                _lib.load().mgrit_loop_destroy(self.handle)
-            except Exception:  # interpreter shutdown: the library may be gone
-                pass
+            _DEAD_LOOPS.append(self.handle)
             self.handle = None
 
 
@@ -821,6 +831,7 @@ def _solve_loop(sess: _Session, cfg: SolverConfig, status: torch.Tensor) -> _Loo
     if sess.loop is not None and sess.loop.hist.numel() > cfg.max_iters:
         return sess.loop
     sess.loop = None
+    _flush_loops()
     lib = _lib.load()
     dev = sess.U.device
     eng = sess.engine
@@ -831,17 +842,23 @@ def _solve_loop(sess: _Session, cfg: SolverConfig, status: torch.Tensor) -> _Loo
     side = torch.cuda.Stream(device=dev)   # the legacy default stream cannot be captured
     side.wait_stream(cur)
     h = ctypes.c_void_p()
-    with torch.cuda.stream(side):
-        sp = stream_ptr()
-        _lib.check(lib.mgrit_loop_begin(sp, ctypes.byref(h)), "loop_begin")
-        try:
-            eng.iteration()
-            _lib.check(lib.mgrit_loop_check(h, eng.sumsq.data_ptr(), status.data_ptr(), hist.data_ptr(),
-                                            ctrl.data_ptr(), par.data_ptr(), sp), "loop_check")
-            _lib.check(lib.mgrit_loop_end(h, sp), "loop_end")
-        except Exception:
-            lib.mgrit_loop_destroy(h)
-            raise
+    gc_was_enabled = gc.isenabled()
+    gc.disable()   # no finalisers (CUDA frees) on this thread while capturing
+    try:
+        with torch.cuda.stream(side):
+            sp = stream_ptr()
+            _lib.check(lib.mgrit_loop_begin(sp, ctypes.byref(h)), "loop_begin")
+            try:
+                eng.iteration()
+                _lib.check(lib.mgrit_loop_check(h, eng.sumsq.data_ptr(), status.data_ptr(), hist.data_ptr(),
+                                                ctrl.data_ptr(), par.data_ptr(), sp), "loop_check")
+                _lib.check(lib.mgrit_loop_end(h, sp), "loop_end")
+            except Exception:
+                lib.mgrit_loop_destroy(h)
+                raise
+    finally:
+        if gc_was_enabled:
+            gc.enable()
     cur.wait_stream(side)
     sess.loop = _Loop(h, hist, ctrl, par)
     return sess.loop
