@@ -234,7 +234,7 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                     if (F || i < n) b0[i] = v[k];
                 }
             }
-            double g_k = beta;  // thread 0: running g[kk] of the least-squares rhs
+            double g_k = beta;  // running g[kk] of the least-squares rhs (every thread)
             int done = 0;
 #pragma unroll 1
             for (int kk = 0; kk < K; ++kk) {
@@ -258,7 +258,7 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 // Thread 0 applies the previous Givens rotations to column kk as
                 // its entries arrive (rotation j needs h_j and h_{j+1} only), in
                 // the reference's order.
-                double hrun = 0.0;  // thread 0: column kk entry j after rotations < j
+                double hrun = 0.0;  // column kk entry j after rotations < j (every thread)
                 double bc[NPT];
                 {
                     const double *b0p = kk == 0 ? cx.rowbuf : cx.bvec(0, n);
@@ -296,22 +296,22 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                     for (int k = 0; k < NPT; ++k) a4[k & 3] = fma(cur[k], v[k], a4[k & 3]);
                     const double part = __dadd_rn(__dadd_rn(a4[0], a4[1]), __dadd_rn(a4[2], a4[3]));
                     double c = 0.0, sn = 0.0;
-                    if (tid == 0 && j > 0) {
+                    if (j > 0) {
                         c = G.cs[j - 1];
                         sn = G.sn[j - 1];
                     }
                     if (kk == 5) MGRIT_PROBE_AT(301 + 4 * j);
                     const double h = block_sum2<NT>(part, cx);
                     if (kk == 5) MGRIT_PROBE_AT(302 + 4 * j);
-                    if (tid == 0) {
-                        if (j == 0) {
-                            hrun = h;
-                        } else {
-                            // rotation j-1 on rows (j-1, j) of column kk
-                            const double tmp = __dadd_rn(__dmul_rn(c, hrun), __dmul_rn(sn, h));
-                            hrun = __dadd_rn(__dmul_rn(-sn, hrun), __dmul_rn(c, h));
-                            G.H[(j - 1) * kMaxKrylov + kk] = tmp;
-                        }
+                    // every thread applies the rotations (identical inputs ->
+                    // identical values), so the stop test needs no barrier
+                    if (j == 0) {
+                        hrun = h;
+                    } else {
+                        // rotation j-1 on rows (j-1, j) of column kk
+                        const double tmp = __dadd_rn(__dmul_rn(c, hrun), __dmul_rn(sn, h));
+                        hrun = __dadd_rn(__dmul_rn(-sn, hrun), __dmul_rn(c, h));
+                        if (tid == 0) G.H[(j - 1) * kMaxKrylov + kk] = tmp;
                     }
 #pragma unroll
                     for (int k = 0; k < NPT; ++k) v[k] = fma(-h, cur[k], v[k]);
@@ -332,24 +332,26 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 const double nrm = sqrt(block_sum2<NT>(sumsq4(), cx));
                 MGRIT_PROBE_AT(13 + 8 * kk);
                 const bool brk = nrm <= __dmul_rn(1e-14, beta);
-                // b_{kk+1} = w / h_{kk+1,kk}, written even on breakdown (the
-                // slot is then never read), so no branch separates it from
-                // thread 0's rotation below
-                if (tid == 0) {
-                    // new rotation from (H[kk][kk], h_{kk+1,kk} = nrm); the
-                    // divisions are reciprocal + Markstein correction
-                    // (correctly rounded, = hess / denom)
+                // new rotation from (H[kk][kk], h_{kk+1,kk} = nrm), evaluated
+                // by every thread; the divisions are reciprocal + Markstein
+                // correction (correctly rounded, = hess / denom).  b_{kk+1} =
+                // w / h_{kk+1,kk} below is written even on breakdown (the slot
+                // is then never read), so no branch separates the two chains.
+                bool stop;
+                {
                     const double den = hypot(hrun, nrm);
                     const double rden = __drcp_rn(den);
                     const double c = div_rcp(hrun, den, rden), sn = div_rcp(nrm, den, rden);
-                    G.cs[kk] = c;
-                    G.sn[kk] = sn;
-                    G.H[kk * kMaxKrylov + kk] = den;
                     const double gn = __dmul_rn(-sn, g_k);
-                    G.g[kk] = __dmul_rn(c, g_k);
-                    G.g[kk + 1] = gn;
+                    if (tid == 0) {
+                        G.cs[kk] = c;
+                        G.sn[kk] = sn;
+                        G.H[kk * kMaxKrylov + kk] = den;
+                        G.g[kk] = __dmul_rn(c, g_k);
+                        G.g[kk + 1] = gn;
+                    }
                     g_k = gn;
-                    G.stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta));
+                    stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta));
                 }
                 MGRIT_PROBE_AT(14 + 8 * kk);
                 {
@@ -364,10 +366,10 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                 }
                 MGRIT_PROBE_AT(15 + 8 * kk);
                 done = kk + 1;
-                __syncthreads();
                 MGRIT_PROBE_AT(16 + 8 * kk);
-                if (G.stop) break;
+                if (stop) break;
             }
+            __syncthreads();  // G.H / G.g from thread 0
             // back substitution on warp 0 (column-oriented, as LAPACK trsv):
             // lane i keeps acc_i = g_i - sum_{j>i} H[i][j] y_j
             if (tid < 32) {
