@@ -52,8 +52,9 @@ __device__ __forceinline__ Dec decompose_s(double s, int n) {
         ef = __dadd_rn(ef, 1.0);
         e += 1;
     }
+    // ef = ceil(s) >= s, so RN(ef - s) >= 0: the reference's "eps < 0 -> 0"
+    // guard (semi_lagrangian.py:131) can never fire here and is omitted
     double eps = __dsub_rn(ef, s);
-    if (eps < 0.0) eps = 0.0;
     if (eps >= 1.0) {
         eps = __dsub_rn(eps, 1.0);
         e -= 1;

@@ -226,23 +226,33 @@ __device__ __forceinline__ double pcg_double(u128 st) {
     return (double)(out >> 11) * (1.0 / 9007199254740992.0);
 }
 
-constexpr int64_t kPcgChunk = 64;
+// Warp-interleaved generation: a warp owns kPcgWarpBlock consecutive draws;
+// lane l produces draws base + l, base + l + 32, ... by jumping its state 32
+// steps at a time (x -> A32 x + C32, the affine map of 32 LCG steps), so
+// every store instruction of the warp writes 32 consecutive doubles.
+constexpr int64_t kPcgWarpBlock = 32 * 64;
 
 __global__ void pcg64_kernel(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, int64_t count,
                              int pm1, double *out) {
     const u128 state0 = ((u128)sh << 64) | sl;
     const u128 inc = ((u128)ih << 64) | il;
-    const int64_t chunks = (count + kPcgChunk - 1) / kPcgChunk;
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < chunks;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t first = c * kPcgChunk;
-        u128 st = pcg_advance(state0, inc, (uint64_t)first);
-        const int64_t last = first + kPcgChunk < count ? first + kPcgChunk : count;
-        for (int64_t k = first; k < last; ++k) {
-            st = st * pcg_mult() + inc;  // step, then output (pcg_setseq_128_xsl_rr_64)
+    // affine map of 32 steps: advance(x, 32) = a32 * x + c32
+    const u128 c32 = pcg_advance(0, inc, 32);
+    const u128 a32 = pcg_advance(1, inc, 32) - c32;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t blocks = (count + kPcgWarpBlock - 1) / kPcgWarpBlock;
+    for (int64_t wb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wb < blocks; wb += warps_total) {
+        const int64_t base = wb * kPcgWarpBlock;
+        int64_t k = base + lane;
+        // state after draw k's step (numpy steps, then outputs)
+        u128 st = pcg_advance(state0, inc, (uint64_t)k + 1);
+        const int64_t end = base + kPcgWarpBlock < count ? base + kPcgWarpBlock : count;
+        for (; k < end; k += 32) {
             double v = pcg_double(st);
             if (pm1) v = __dsub_rn(__dmul_rn(2.0, v), 1.0);
             out[k] = v;
+            st = a32 * st + c32;
         }
     }
 }
@@ -329,8 +339,8 @@ extern "C" int mgrit_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t i
                                 void *stream) {
     if (count < 0 || (count > 0 && !out)) return MGRIT_EINVAL;
     if (count == 0) return MGRIT_OK;
-    const int64_t chunks = (count + kPcgChunk - 1) / kPcgChunk;
-    pcg64_kernel<<<grid_for(chunks), kSetupThreads, 0, (cudaStream_t)stream>>>(
+    const int64_t blocks = (count + kPcgWarpBlock - 1) / kPcgWarpBlock;
+    pcg64_kernel<<<grid_for(blocks * 32), kSetupThreads, 0, (cudaStream_t)stream>>>(
         state_hi, state_lo, inc_hi, inc_lo, count, pm1, out);
     return check_launch("pcg64_fill");
 }
