@@ -6,8 +6,10 @@
 // three coarsest levels), so the one-CTA-per-chain kernel leaves >90% of the
 // 148 SMs idle and every Arnoldi step is bound by one SM's shared-memory
 // bandwidth (a 32 KB basis vector per projection) plus a block reduction.
-// Splitting the row over an 8-CTA cluster gives each SM a 512-node chunk;
-// reductions become cluster all-reduces over DSMEM:
+// Splitting the row over a CS-CTA cluster (CS = 2, 4, 8 or 16, picked per
+// level from measured costs, step1d_cl.cu) gives each SM an n/CS-node chunk
+// (512 nodes at n = 4096, CS = 8); reductions become cluster all-reduces over
+// DSMEM:
 //   * every CTA reduces its partials, st.async-pushes them into every peer's
 //     receive slot (mbarrier complete_tx), waits on its own mbarrier and sums
 //     the CS contributions in rank order -> bit-identical totals in all CTAs,
@@ -120,8 +122,9 @@ struct ClCtx {
 };
 
 // GG ("global gather"): rows too large for a shared-memory copy next to the
-// Krylov chunks (n = 16384) are gathered straight from L2; publication is
-// then a cluster barrier (release / acquire) instead of a TMA multicast.
+// Krylov chunks (n = 16384 at CS = 8 or 16) are gathered straight from L2;
+// publication is then a cluster barrier (release / acquire) instead of a TMA
+// multicast.
 // (decided for the largest Krylov space, kMaxKrylovCl + 1 chunk slots)
 constexpr size_t kClSmemMax = 227 * 1024;
 template <int CS>
