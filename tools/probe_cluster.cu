@@ -23,6 +23,7 @@ int main(int argc, char **argv) {
     const int K = argc > 2 ? atoi(argv[2]) : 10;
     const int lowsync = argc > 3 ? atoi(argv[3]) : 0;
     const int steps = argc > 4 ? atoi(argv[4]) : 1;
+    const int csz = argc > 5 ? atoi(argv[5]) : 8;   // cluster size 2 / 4 / 8 / 16
     std::vector<double> s(n), sig(n), u((steps + 1) * n, 0.0);
     srand(1);
     for (int i = 0; i < n; ++i) {
@@ -42,13 +43,17 @@ int main(int argc, char **argv) {
     L.s_x = ds; L.sig_x = dsig; L.gmres_max_iters = K; L.gmres_tol = -1.0; L.gmres_lowsync = lowsync;
     for (int rep = 0; rep < 3; ++rep) {
         cudaMemcpy(du, u.data(), (steps + 1) * n * 8, cudaMemcpyHostToDevice);
-        int rc = cl::LaunchCl<3, 8>::sweep(&L, du, n, nullptr, 0, 0, nullptr, st, 0);
+        int rc = csz == 2 ? cl::LaunchCl<3, 2>::sweep(&L, du, n, nullptr, 0, 0, nullptr, st, 0)
+               : csz == 4 ? cl::LaunchCl<3, 4>::sweep(&L, du, n, nullptr, 0, 0, nullptr, st, 0)
+               : csz == 16 ? cl::LaunchCl<3, 16>::sweep(&L, du, n, nullptr, 0, 0, nullptr, st, 0)
+                           : cl::LaunchCl<3, 8>::sweep(&L, du, n, nullptr, 0, 0, nullptr, st, 0);
         if (rc) { printf("launch rc %d\n", rc); return 1; }
     }
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
     long long h[512];
     cudaMemcpyFromSymbol(h, g_probe, sizeof(h));
+    printf("CS=%d ", csz);
     printf("n=%d K=%d lowsync=%d steps=%d  await_row %lld  SL+sig %lld  beta %lld  b0 %lld\n", n, K, lowsync, steps, h[401] - h[400],
            h[402] - h[401], h[403] - h[402], h[404] - h[403]);
     for (int kk = 0; kk < K; ++kk) {
