@@ -311,6 +311,23 @@ def run_gpu(args):
                 "traffic": _ncu_traffic(args.config, top), "bytes_per_launch": tb["bytes"],
                 "ms_per_launch": round(tb["ms_avg"], 5), "peak_source": peak["source"],
                 "share_of_iteration": round(tb["ms_total"] / sum(v["ms_total"] for v in breakdown.values()), 3)}
+    if "corrected" in top and cfg.dim == 1 and "sweep" not in top:
+        # the latency view of a corrected phase: when its row chains fit in
+        # one wave, the launch time is steps-per-chain dependent corrected
+        # steps (a level with more chains than resident CTAs / clusters runs
+        # several waves, and the per-step figure is an upper bound)
+        li = int(top[1:].split("_")[0])
+        m = levels[li].cf
+        steps = m - 1 if "INJ_F" in top else m
+        us_step = tb["ms_avg"] * 1e3 / steps
+        roofline["latency"] = {
+            "row_chains": levels[li].n_steps // m, "steps_per_chain": steps,
+            "us_per_corrected_step": round(us_step, 2),
+            "cycles_per_corrected_step_at_1965MHz": int(us_step * 1965),
+            "note": "each corrected step is an SL gather + MGS-GMRES with up to 10 Arnoldi steps; "
+                    "every MGS projection is one cluster all-reduce (~580 cycles: fp64 warp butterfly "
+                    "~200 + DSMEM round trip ~300, clock64 probe), so the step is bound by ~K^2/2 "
+                    "dependent all-reduces, not by bytes"}
 
     # the SL-step kernel itself (BASELINE: "SL-step HBM GB/s"): the fine-level
     # F+C relaxation phase (plain semi-Lagrangian steps, G = 0)
