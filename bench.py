@@ -373,7 +373,9 @@ def run_gpu(args):
     del Useq
 
     iters = rep.iterations
-    launches = 3 + 2 + launches_iter * iters      # pcg fill + r0 (rows + sum) + per-iteration
+    # pcg fill + r0 (rows + sum) + loop init, then per iteration the V-cycle
+    # launches, the norm sum and the device loop's stop test
+    launches = 3 + 1 + (launches_iter + 1) * iters if world == 1 else 3 + launches_iter * iters
     parity = None
     gold = _golden(args.config)
     if gold is not None:
