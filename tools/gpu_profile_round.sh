@@ -1,7 +1,7 @@
 #!/bin/bash
 # cfg2 bench launch list + ncu --set full captures of the fine SL phase and the
 # top coarse phase (tools only; run under gpurun, one GPU).  TAG names the files.
-TAG=${TAG:-r01d}
+TAG=${TAG:-r01e}
 mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
   --log-file gpurun_out/${TAG}_launches_bench.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_list.log 2>&1
