@@ -80,11 +80,11 @@ int cl_wave_cost100(int cs, int n) {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / (b > 0 ? b : 1); }
 
-}  // namespace
-
 int cl_resident(const mgrit_level_desc *L, int cs) {
     return by_p_cs(L->p, cs, [&](auto X) { return decltype(X)::resident_clusters(L); });
 }
+
+}  // namespace
 
 // -1: not taken (caller uses the one-CTA kernels)
 int cl_level_phase(const mgrit_level_desc *L, const mgrit_phase_args *A, int32_t *status, cudaStream_t st) {

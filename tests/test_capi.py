@@ -51,6 +51,24 @@ def test_loop_entry_points_reject_bad_arguments():
     lib.mgrit_loop_destroy(None)
 
 
+def test_launch_policy_names_match_header():
+    """Python launch-policy names map onto the header's MGRIT_LAUNCH_* values
+    (the C side reads the integer from the level descriptor)."""
+    import re as _re
+    from paper_2203_13382_b200 import mgrit as M
+    src = open(HEADER).read()
+    vals = {k: int(v) for k, v in _re.findall(r"MGRIT_LAUNCH_([A-Z0-9_]+)\s*=\s*(\d+)", src)}
+    want = {"auto": "AUTO", "cta": "CTA", "cluster": "CLUSTER", "auto_one": "AUTO_ONE",
+            "cluster2": "CLUSTER2", "cluster4": "CLUSTER4", "cluster8": "CLUSTER8", "cluster16": "CLUSTER16"}
+    assert set(M.LAUNCH_POLICIES) == set(want)
+    for name, enum in want.items():
+        assert M.LAUNCH_POLICIES[name] == vals[enum], name
+    prev = M.set_launch_policy("cluster16")
+    assert M.set_launch_policy(prev) == "cluster16"
+    with pytest.raises(ValueError):
+        M.set_launch_policy("cluster3")
+
+
 def test_library_is_sm100a():
     from paper_2203_13382_b200 import _lib
     r = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
