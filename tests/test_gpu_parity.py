@@ -334,6 +334,27 @@ def test_cfg2_full_size_matches_reference(P, golden_index):
     assert np.allclose(np.linalg.norm(U, axis=1), g["row_norms"], rtol=1e-12, atol=0)
 
 
+@pytest.mark.slow
+def test_two_ctas_per_sm_phase_is_bit_identical(P, golden_index):
+    """cfg2's level 1 (256 row chains) runs two corrected-phase CTAs per SM
+    (sigma re-read from L1, no register prefetch of b_j, two shared-memory
+    Krylov slots) under "auto" and one per SM in two waves under "auto_one":
+    the same arithmetic, so the solves agree bit for bit."""
+    info = golden_index["cfg2_full"]
+    cfg = P.SolverConfig(**info["kw"])
+    levels = P.build_hierarchy(cfg)
+    prev = P.set_launch_policy("auto")
+    try:
+        r1, U1 = P.solve(cfg, levels)
+        P.set_launch_policy("auto_one")
+        r2, U2 = P.solve(cfg, levels)
+    finally:
+        P.set_launch_policy(prev)
+    assert r1.iterations == r2.iterations == info["iterations"]
+    assert np.array_equal(r1.residual_norms, r2.residual_norms)
+    assert np.array_equal(U1, U2)
+
+
 @pytest.mark.parametrize("name", ["tiny1d_C3_p3_m4", "tiny1d_B2_p5_m8", "tiny1d_C1_2lvl_pm1"])
 def test_per_iteration_snapshots(P, golden_index, name):
     """Iterates after every V-cycle within relative 1e-12 of the reference's
