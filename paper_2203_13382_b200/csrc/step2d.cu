@@ -161,7 +161,10 @@ struct SL2DMinBlocks {
     static constexpr int value = P == 5 ? 4 : 8;
 };
 
-template <int P, bool SLONLY, int MINB, bool PREF>
+// FULL: n is a multiple of the 1024-node tile (every BASELINE 2D mesh), so the
+// per-node bounds checks compile away.  Used for p = 5 (cfg5 F-step 4.95 ->
+// 4.69 ms); at p = 3 the 32-register build spills more with it and was slower.
+template <int P, bool SLONLY, int MINB, bool PREF, bool FULL = false>
 __global__ void __launch_bounds__(kNT2, MINB) sl2d_kernel(mgrit_level_desc L, Rows2D a) {
     __shared__ double red[kNT2 / 32 + 1];
     const int nx = L.n_x;
@@ -169,7 +172,8 @@ __global__ void __launch_bounds__(kNT2, MINB) sl2d_kernel(mgrit_level_desc L, Ro
     const int64_t b = blockIdx.y;
     const int64_t t = row_t(a, b);
     const int64_t set = L.shared ? 0 : t;
-    const double *sx = L.s_x + set * n, *sy = L.s_y + set * n;
+    const int64_t tile0 = (int64_t)blockIdx.x * kTile2 + threadIdx.x;
+    const double *sx = L.s_x + set * n + tile0, *sy = L.s_y + set * n + tile0;
     const double *u = a.U_in + b * a.ld_in;
     double ss = 0.0;
     constexpr int NK = kTile2 / kNT2;
@@ -177,16 +181,17 @@ __global__ void __launch_bounds__(kNT2, MINB) sl2d_kernel(mgrit_level_desc L, Ro
     if constexpr (PREF) {
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
-            const int64_t i = (int64_t)blockIdx.x * kTile2 + k * kNT2 + threadIdx.x;
-            rx[k] = i < n ? __ldcs(sx + i) : 0.0;
-            ry[k] = i < n ? __ldcs(sy + i) : 0.0;
+            const bool in = FULL || tile0 + k * kNT2 < n;
+            rx[k] = in ? __ldcs(sx + k * kNT2) : 0.0;
+            ry[k] = in ? __ldcs(sy + k * kNT2) : 0.0;
         }
     }
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
-        const int64_t i = (int64_t)blockIdx.x * kTile2 + k * kNT2 + threadIdx.x;
-        if (i < n) {
-            double v = PREF ? sl2d_at<P>(u, nx, rx[k], ry[k]) : sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
+        const int64_t i = tile0 + k * kNT2;
+        if (FULL || i < n) {
+            double v = PREF ? sl2d_at<P>(u, nx, rx[k], ry[k])
+                            : sl2d_at<P>(u, nx, __ldg(sx + k * kNT2), __ldg(sy + k * kNT2));
             if constexpr (!SLONLY) {
                 const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
                 if (a.U_sub) {
@@ -671,14 +676,20 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             Rows2D s = a;
             s.out = V;
             s.ld_out = n;
-            sl2d_kernel<P, true, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
+            if (P == 5 && n % kTile2 == 0)
+                sl2d_kernel<P, true, SL2DMinBlocks<P>::value, true, P == 5><<<grid, kNT2, 0, st>>>(*L, s);
+            else
+                sl2d_kernel<P, true, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
             Rows2D f = a;
             f.partial = partial;
             fe2d_kernel<P><<<grid, kNT2, 0, st>>>(*L, f, V);
         } else {
             Rows2D s = a;
             s.partial = partial;
-            sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
+            if (P == 5 && n % kTile2 == 0)
+                sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true, P == 5><<<grid, kNT2, 0, st>>>(*L, s);
+            else
+                sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
         }
         if (partial) rowsum_kernel<<<(unsigned)(r.B < 4096 ? r.B : 4096), kNT2, 0, st>>>(partial, tiles, r.B, r.row_sumsq);
         return check_launch("apply_rows_2d");
