@@ -36,8 +36,11 @@ __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >
 
 // 2D SL value at node (ix, iy): semi_lagrangian.py:238-253 (x inner, y outer,
 // both accumulators start at 0, separately rounded products)
-template <int P>
-__device__ __forceinline__ double sl2d_at(const double *u, int nx, double sx, double sy) {
+// NX > 0: the mesh width as a compile-time constant (512, 1024: the BASELINE
+// meshes), so the row stride of the tap window is an immediate offset
+template <int P, int NX = 0>
+__device__ __forceinline__ double sl2d_at(const double *u, int nx_rt, double sx, double sy) {
+    const int nx = NX > 0 ? NX : nx_rt;
     constexpr int SL = Stencil<P>::L;
     const Dec dx = decompose_s(sx, nx);
     const Dec dy = decompose_s(sy, nx);
@@ -50,12 +53,23 @@ __device__ __forceinline__ double sl2d_at(const double *u, int nx, double sx, do
         // interior window (almost every node): one base address, the taps
         // are immediate offsets from it and one row stride
         const double *r = u + (int64_t)(dy.e - SL) * nx + (dx.e - SL);
+        if constexpr (NX > 0) {
 #pragma unroll
-        for (int jy = 0; jy <= P; ++jy, r += nx) {
-            double acc = 0.0;
+            for (int jy = 0; jy <= P; ++jy) {
+                double acc = 0.0;
 #pragma unroll
-            for (int jx = 0; jx <= P; ++jx) acc = __dadd_rn(acc, __dmul_rn(wx[jx], __ldg(r + jx)));
-            out = __dadd_rn(out, __dmul_rn(wy[jy], acc));
+                for (int jx = 0; jx <= P; ++jx)
+                    acc = __dadd_rn(acc, __dmul_rn(wx[jx], __ldg(r + jy * NX + jx)));  // immediate offsets
+                out = __dadd_rn(out, __dmul_rn(wy[jy], acc));
+            }
+        } else {
+#pragma unroll
+            for (int jy = 0; jy <= P; ++jy, r += nx) {
+                double acc = 0.0;
+#pragma unroll
+                for (int jx = 0; jx <= P; ++jx) acc = __dadd_rn(acc, __dmul_rn(wx[jx], __ldg(r + jx)));
+                out = __dadd_rn(out, __dmul_rn(wy[jy], acc));
+            }
         }
         return out;
     }
@@ -164,7 +178,7 @@ struct SL2DMinBlocks {
 // FULL: n is a multiple of the 1024-node tile (every BASELINE 2D mesh), so the
 // per-node bounds checks compile away.  Used for p = 5 (cfg5 F-step 4.95 ->
 // 4.69 ms); at p = 3 the 32-register build spills more with it and was slower.
-template <int P, bool SLONLY, int MINB, bool PREF, bool FULL = false>
+template <int P, bool SLONLY, int MINB, bool PREF, bool FULL = false, int NX = 0>
 __global__ void __launch_bounds__(kNT2, MINB) sl2d_kernel(mgrit_level_desc L, Rows2D a) {
     __shared__ double red[kNT2 / 32 + 1];
     const int nx = L.n_x;
@@ -190,8 +204,8 @@ __global__ void __launch_bounds__(kNT2, MINB) sl2d_kernel(mgrit_level_desc L, Ro
     for (int k = 0; k < NK; ++k) {
         const int64_t i = tile0 + k * kNT2;
         if (FULL || i < n) {
-            double v = PREF ? sl2d_at<P>(u, nx, rx[k], ry[k])
-                            : sl2d_at<P>(u, nx, __ldg(sx + k * kNT2), __ldg(sy + k * kNT2));
+            double v = PREF ? sl2d_at<P, NX>(u, nx, rx[k], ry[k])
+                            : sl2d_at<P, NX>(u, nx, __ldg(sx + k * kNT2), __ldg(sy + k * kNT2));
             if constexpr (!SLONLY) {
                 const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
                 if (a.U_sub) {
@@ -686,7 +700,12 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
         } else {
             Rows2D s = a;
             s.partial = partial;
-            if (P == 5 && n % kTile2 == 0)
+            // p = 3 on the 512-wide mesh (cfg4): the tap rows are immediate
+            // offsets from one base pointer (0.676 -> 0.618 ms per F-step);
+            // at p = 5 the same form measured slower (4.69 -> 4.91 ms)
+            if (P == 3 && L->n_x == 512)
+                sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true, false, 512><<<grid, kNT2, 0, st>>>(*L, s);
+            else if (P == 5 && n % kTile2 == 0)
                 sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true, P == 5><<<grid, kNT2, 0, st>>>(*L, s);
             else
                 sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);

@@ -505,13 +505,14 @@ def test_sl_step_batch_2d_bitwise(P, p, speed):
     assert np.array_equal(_np(Rd), O.residual(olevels[0], U0, G))
 
 
-@pytest.mark.parametrize("p", [1, 3, 5])
+@pytest.mark.parametrize("p,nx", [(1, 256), (3, 256), (5, 256), (3, 512)])
 @pytest.mark.parametrize("speed,cfl", [("B4", 0.85), ("C5", 0.85), ("B4", 100.0)])
-def test_sl_step_batch_2d_large_mesh_bitwise(P, p, speed, cfl):
-    """A 256^2 mesh (interior fast path on most nodes, wrapped windows at the
-    edges), including dt = 100h whose departures wrap around the domain:
-    step_batch / f_relax / residual bit-identical to the reference."""
-    nx = 256
+def test_sl_step_batch_2d_large_mesh_bitwise(P, p, nx, speed, cfl):
+    """256^2 and 512^2 meshes (interior fast path on most nodes, wrapped
+    windows at the edges; 512^2 at p = 3 is config 4's mesh and runs the
+    kernel specialised for that width), including dt = 100h whose departures
+    wrap around the domain: step_batch / f_relax / residual bit-identical to
+    the reference."""
     kw = dict(n_x=nx, n_t=8, dim=2, wave_speed=speed, p=p, schedule=4, dt=cfl * 2.0 / nx)
     cfg, ocfg = _cfg_pair(P, kw)
     coords, olevels = _fine_coords(ocfg)
