@@ -301,7 +301,7 @@ struct CoopSmem {
     int stop;
 };
 
-template <int P>
+template <int P, int NX = 0>
 __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     __shared__ CoopSmem S;
     const mgrit_level_desc &L = C.L;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
         {
             const double *u = a.U_in + b * a.ld_in;
             for_nodes_red([&](int64_t i, int ix, int iy) {
-                const double v = sl2d_at<P>(u, nx, __ldg(sx + i), __ldg(sy + i));
+                const double v = sl2d_at<P, NX>(u, nx, __ldg(sx + i), __ldg(sy + i));
                 src[i] = v;
                 if (!isfinite(v)) bad = 1;
                 return __dmul_rn(v, v);
@@ -633,7 +633,10 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
     if (L->kind == MGRIT_KIND_CORRECTED) {
         return dispatch_p(L->p, [&](auto PP) {
             constexpr int P = decltype(PP)::value;
-            const void *fn = (const void *)gmres2d_coop<P>;
+            // p = 3 on the 512-wide mesh: the SL pass with immediate tap-row
+            // offsets, as sl2d_kernel (same arithmetic, same capacity)
+            const void *fn = (P == 3 && L->n_x == 512) ? (const void *)gmres2d_coop<P, (P == 3 ? 512 : 0)>
+                                                       : (const void *)gmres2d_coop<P>;
             const int G = coop_capacity(fn);
             int64_t rows = r.B < G ? r.B : G;
             const int64_t cap = coop_rows_cap(L);
