@@ -118,9 +118,10 @@ __device__ __forceinline__ double imsd2d_at(const double *v, int nx, int ix, int
 // normalisation b_j = w / h would store it (div_rcp, = RN(v / s)); also
 // returns b at the node itself.  Lets the GMRES stencil pass read the
 // un-normalised Arnoldi vector and write b_kk on the fly (no separate pass).
-template <int P>
-__device__ __forceinline__ double imsd2d_scaled(const double *v, int nx, int ix, int iy, double sx, double sy,
+template <int P, int NX = 0>
+__device__ __forceinline__ double imsd2d_scaled(const double *v, int nx_rt, int ix, int iy, double sx, double sy,
                                                 double s, double rs, double &bi) {
+    const int nx = NX > 0 ? NX : nx_rt;
     constexpr int RAD = (P + 1) / 2;
     const double *row = v + (int64_t)iy * nx;
     auto bq = [&](double x) { return div_rcp(x, s, rs); };
@@ -132,8 +133,8 @@ __device__ __forceinline__ double imsd2d_scaled(const double *v, int nx, int ix,
 #pragma unroll
         for (int q = 1; q <= RAD; ++q) {
             dx = __dadd_rn(__dadd_rn(dx, cmul<P>(RAD + q, bq(c[q]))), cmul<P>(RAD - q, bq(c[-q])));
-            dy = __dadd_rn(__dadd_rn(dy, cmul<P>(RAD + q, bq(c[(int64_t)q * nx]))),
-                           cmul<P>(RAD - q, bq(c[-(int64_t)q * nx])));
+            const int64_t qn = NX > 0 ? (int64_t)q * NX : (int64_t)q * nx;
+            dy = __dadd_rn(__dadd_rn(dy, cmul<P>(RAD + q, bq(c[qn]))), cmul<P>(RAD - q, bq(c[-qn])));
         }
         return __dsub_rn(__dsub_rn(vi, __dmul_rn(sx, dx)), __dmul_rn(sy, dy));
     }
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             // b_kk, w = A b_kk ; inner product with b_0
             for_nodes_red([&](int64_t i, int ix, int iy) {
                 double bi;
-                const double x = imsd2d_scaled<P>(src, nx, ix, iy, __ldg(gx + i), __ldg(gy + i), scale, rscale, bi);
+                const double x = imsd2d_scaled<P, NX>(src, nx, ix, iy, __ldg(gx + i), __ldg(gy + i), scale, rscale, bi);
                 bk[i] = bi;
                 dst[i] = x;
                 return __dmul_rn(kk == 0 ? bi : basis[i], x);
