@@ -636,8 +636,9 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             constexpr int P = decltype(PP)::value;
             // p = 3 on the 512-wide mesh: the SL pass with immediate tap-row
             // offsets, as sl2d_kernel (same arithmetic, same capacity)
-            const void *fn = (P == 3 && L->n_x == 512) ? (const void *)gmres2d_coop<P, (P == 3 ? 512 : 0)>
-                                                       : (const void *)gmres2d_coop<P>;
+            const void *fn = (P == 3 && L->n_x == 512)    ? (const void *)gmres2d_coop<P, (P == 3 ? 512 : 0)>
+                             : (P == 5 && L->n_x == 1024) ? (const void *)gmres2d_coop<P, (P == 5 ? 1024 : 0)>
+                                                          : (const void *)gmres2d_coop<P>;
             const int G = coop_capacity(fn);
             int64_t rows = r.B < G ? r.B : G;
             const int64_t cap = coop_rows_cap(L);
