@@ -455,10 +455,18 @@ def kernel_breakdown(levels, cfg, inner: int = 5, reps: int = 3):
     from paper_2203_13382_b200 import mgrit as M
     dev = torch.device("cuda")
     U = torch.empty((cfg.n_t + 1, levels[0].grid.n_points), dtype=torch.float64, device=dev)
-    U[0] = 0.5
+    # the solve's own first iterate (u0 row + seeded PCG64 rows): corrected
+    # steps stop GMRES early on breakdown or tolerance, so their cost depends
+    # on the data
+    U[0] = torch.from_numpy(M.initial_state(cfg, levels[0].grid)).to(dev)
     M.pcg64_uniform(cfg.seed, cfg.n_t, levels[0].grid.n_points, U[1:])
     eng = M._FusedCycle(levels, U, cfg.relaxation)
-    eng.iteration()                     # realistic state + kernel attributes set
+    eng.iteration()                     # kernel attributes set, buffers touched
+    # back to the first iterate, so every phase below sees the data of the
+    # solve's first V-cycle (after a converged cycle the coarse right-hand
+    # sides are tiny and the corrected steps would run all K Arnoldi steps)
+    U[0] = torch.from_numpy(M.initial_state(cfg, levels[0].grid)).to(dev)
+    M.pcg64_uniform(cfg.seed, cfg.n_t, levels[0].grid.n_points, U[1:])
     torch.cuda.synchronize()
     names = {_lib.PHASE_FC: "FC", _lib.PHASE_F_RES: "F_RES", _lib.PHASE_FONLY_RES: "FONLY_RES",
              _lib.PHASE_INJ_F: "INJ_F"}
