@@ -249,6 +249,46 @@ int mgrit_loop_init(const double *r0_sumsq, double *hist, int32_t *ctrl, double 
                     void *stream);
 int mgrit_loop_launch(void *loop, void *stream);
 void mgrit_loop_destroy(void *loop);
+/* kernel nodes of the captured body (one V-cycle + stop test); -1 on error */
+int64_t mgrit_loop_body_kernels(void *loop);
+
+/* -------------------------------------- operator-level API below Level --- */
+
+/* decompose(grid, coords) (semi_lagrangian.py:118-137): east index (int64,
+ * wrapped into [0, n_x)) and offset eps in [0, 1) of `count` coordinates on
+ * a periodic [-1, 1) axis of n_x nodes, with the reference's rounding guards. */
+int mgrit_decompose(int32_t n_x, int64_t count, const double *coords, int64_t *east,
+                    double *eps, void *stream);
+
+/* interp_weights(p, eps) (semi_lagrangian.py:140-161): w[count][p+1], the
+ * reference's products and (correctly rounded) divisions. */
+int mgrit_interp_weights(int32_t p, int64_t count, const double *eps, double *w,
+                         void *stream);
+
+/* Records from a reference DepartureSet (DepartureSet1D.east/eps,
+ * DepartureSet2D.east_x/eps and east_y/nu; semi_lagrangian.py:164-205): the
+ * scaled coordinate s = E - eps (E = east, or n_x for east == 0), from which
+ * the device re-derives exactly the given (east, eps) — a records-based entry
+ * for callers that hold DepartureSets instead of coordinates. */
+int mgrit_records_from_east_eps(int32_t n_x, int64_t count, const int64_t *east,
+                                const double *eps, double *s, void *stream);
+
+/* apply_ImSD(field, derivative_stencil(p), v, grid) (coarse_correction.py:
+ * 130-149) on `rows` vectors sharing one field: out = (I - diag(sx) Dx
+ * [- diag(sy) Dy]) v, the reference's grouping, separately rounded. */
+int mgrit_apply_imsd(int32_t dim, int32_t n_x, int32_t p, int64_t rows,
+                     const double *sig_x, const double *sig_y, const double *v,
+                     int64_t ldv, double *out, int64_t ldo, void *stream);
+
+/* Level.step_batch with the GMRES residual history of every corrected row
+ * (gmres_solve's (x, res_hist) return, coarse_correction.py:173-228):
+ * out[b] = Phi_{t_b} U_in[b]; gmres_hist[b][0..iters[b]] = beta, |g_1|, ...
+ * (gmres_hist: [B][gmres_max_iters + 1], nullable). */
+int mgrit_apply_rows_hist(const mgrit_level_desc *L, int64_t B, const int64_t *t_idx,
+                          int64_t t_first, int64_t t_stride, const double *U_in,
+                          int64_t ld_in, double *out, int64_t ld_out,
+                          int32_t *gmres_iters, double *gmres_hist, void *scratch,
+                          int64_t scratch_bytes, int32_t *status, void *stream);
 
 #ifdef __cplusplus
 }

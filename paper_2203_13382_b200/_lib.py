@@ -76,6 +76,13 @@ _SIGS = {
     "mgrit_loop_init": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_i32, c_vp]),
     "mgrit_loop_launch": (ctypes.c_int, [c_vp, c_vp]),
     "mgrit_loop_destroy": (None, [c_vp]),
+    "mgrit_loop_body_kernels": (c_i64, [c_vp]),
+    "mgrit_decompose": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "mgrit_interp_weights": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, c_vp]),
+    "mgrit_records_from_east_eps": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "mgrit_apply_imsd": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "mgrit_apply_rows_hist": (ctypes.c_int, [ctypes.POINTER(LevelDesc), c_i64, c_vp, c_i64, c_i64, c_vp, c_i64,
+                                             c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
 }
 
 LOOP_STATES = {0: "running", 1: "converged", 2: "diverged", 3: "max_iters"}

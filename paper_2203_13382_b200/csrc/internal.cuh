@@ -14,6 +14,7 @@ struct RowsArgs {
     double *out; int64_t ld_out;
     double *row_sumsq;
     int32_t *gmres_iters;
+    double *gmres_hist = nullptr;   // [B][K+1] GMRES residual histories (corrected rows)
 };
 
 int apply_rows_1d(const mgrit_level_desc *L, const RowsArgs &a, void *scratch,

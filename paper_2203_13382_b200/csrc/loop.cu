@@ -155,3 +155,26 @@ extern "C" void mgrit_loop_destroy(void *loop) {
     if (lp->graph) cudaGraphDestroy(lp->graph);
     delete lp;
 }
+
+// Kernel nodes in the captured loop body (one V-cycle + the stop test): the
+// kernels one iteration of the device-resident solve launches.  Memset /
+// memcpy nodes (2D row copies) are not kernels and are not counted.
+extern "C" int64_t mgrit_loop_body_kernels(void *loop) {
+    Loop *lp = (Loop *)loop;
+    if (!lp || !lp->body || lp->capture) return -1;
+    size_t count = 0;
+    if (cudaGraphGetNodes(lp->body, nullptr, &count) != cudaSuccess) return -1;
+    if (count == 0) return 0;
+    cudaGraphNode_t *nodes = new cudaGraphNode_t[count];
+    int64_t kernels = 0;
+    if (cudaGraphGetNodes(lp->body, nodes, &count) == cudaSuccess) {
+        for (size_t i = 0; i < count; ++i) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++kernels;
+        }
+    } else {
+        kernels = -1;
+    }
+    delete[] nodes;
+    return kernels;
+}

@@ -57,6 +57,7 @@ struct RowCtx {
     int nbs;
     int sel;          // double-buffer parity of the block reductions
     int32_t *status;  // sticky non-finite flag
+    double *hist;     // nullable: GMRES residual history [K+1] of the current row
     __device__ __forceinline__ double *bvec(int j, int n) const {
         return j < nbs ? bsm + (int64_t)j * n : bgl + (int64_t)(j - nbs) * n;
     }
@@ -219,6 +220,7 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
             MGRIT_PROBE_AT(1);
             const double beta = sqrt(block_sum2<NT>(sumsq4(), cx));
             MGRIT_PROBE_AT(2);
+            if (cx.hist && tid == 0) cx.hist[0] = beta;
             if (beta == 0.0) {
 #pragma unroll
                 for (int k = 0; k < NPT; ++k) v[k] = 0.0;
@@ -349,6 +351,7 @@ __device__ int cta_apply(const mgrit_level_desc &L, int64_t t, RowCtx &cx, doubl
                         G.H[kk * kMaxKrylov + kk] = den;
                         G.g[kk] = __dmul_rn(c, g_k);
                         G.g[kk + 1] = gn;
+                        if (cx.hist) cx.hist[kk + 1] = fabs(gn);
                     }
                     g_k = gn;
                     stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta));
@@ -481,6 +484,7 @@ __device__ __forceinline__ RowCtx make_ctx(double *sm, int n, int nbs, double *s
     c.bgl = (scratch && spill > 0) ? scratch + slot * (int64_t)spill * n : nullptr;
     c.sel = 0;
     c.status = status;
+    c.hist = nullptr;
     return c;
 }
 
@@ -499,6 +503,7 @@ __global__ void __launch_bounds__(NT, 1) rows_kernel(mgrit_level_desc L, RowsArg
         load_records<NT, NPT, F>(L, t, sv);
         load_row<NT, NPT, F>(v, a.U_in + b * a.ld_in, n);
         set_row<NT, NPT, F>(cx.rowbuf, v, n);
+        cx.hist = a.gmres_hist ? a.gmres_hist + b * (int64_t)(L.gmres_max_iters + 1) : nullptr;
         const int cnt = cta_apply<P, KIND, NT, NPT, F, false>(L, t, cx, v, sv);
         const double *g = a.G ? a.G + b * a.ld_g : nullptr;
         double ss = 0.0;

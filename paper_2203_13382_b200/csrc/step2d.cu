@@ -157,6 +157,7 @@ struct Rows2D {
     const double *U_sub; int64_t ld_sub;
     double *out; int64_t ld_out;
     double *partial;  // [B][tiles] row sum-of-squares partials (nullable)
+    double *gmres_hist = nullptr;  // [B][K+1] GMRES residual histories (corrected, nullable)
 };
 
 __device__ __forceinline__ int64_t row_t(const Rows2D &a, int64_t b) {
@@ -429,6 +430,8 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
         bad = __syncthreads_or(bad);
         if (tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
         const double beta = sqrt(gtotal());
+        double *hist = (a.gmres_hist && chunk == 0 && tid == 0) ? a.gmres_hist + b * (int64_t)(K + 1) : nullptr;
+        if (hist) hist[0] = beta;
         int anybad = 0;
         if (tid == 0)
             for (int k = 0; k < C.chunks; ++k) anybad |= C.flags[(int64_t)slot * C.chunks + k];
@@ -505,6 +508,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                 const double gn = __dmul_rn(-sn, g_k);
                 S.g[kk] = __dmul_rn(c, g_k);
                 S.g[kk + 1] = gn;
+                if (hist) hist[kk + 1] = fabs(gn);
                 g_k = gn;
                 S.stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta));
             }
@@ -565,12 +569,26 @@ int dispatch_p(int p, Fn &&f) {
 
 }  // namespace
 
+static int64_t coop_rows_cap(const mgrit_level_desc *L);
+
+// the cooperative GMRES instantiation a level dispatches to: p = 3 on the
+// 512-wide mesh and p = 5 on the 1024-wide mesh use compile-time row strides
+static const void *coop_fn(const mgrit_level_desc *L) {
+    switch (L->p) {
+        case 1: return (const void *)gmres2d_coop<1>;
+        case 3: return L->n_x == 512 ? (const void *)gmres2d_coop<3, 512> : (const void *)gmres2d_coop<3>;
+        default: return L->n_x == 1024 ? (const void *)gmres2d_coop<5, 1024> : (const void *)gmres2d_coop<5>;
+    }
+}
+
+// systems the corrected 2D kernel keeps in flight: the L2-sized cap (never
+// more than the cooperative grid holds), so callers size scratch for exactly
+// the rows apply_rows_2d uses
 int64_t capacity2d(const mgrit_level_desc *L) {
     if (L->kind != MGRIT_KIND_CORRECTED) return (int64_t)1 << 30;
-    return dispatch_p(L->p, [&](auto PP) {
-        constexpr int P = decltype(PP)::value;
-        return coop_capacity((const void *)gmres2d_coop<P>);
-    });
+    const int64_t g = coop_capacity(coop_fn(L));
+    const int64_t cap = coop_rows_cap(L);
+    return cap > 0 && cap < g ? cap : g;
 }
 
 // Systems solved concurrently by the cooperative kernel: as many as keep
@@ -632,13 +650,8 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
              r.out, r.ld_out, nullptr};
     char *scr = (char *)scratch;
     if (L->kind == MGRIT_KIND_CORRECTED) {
-        return dispatch_p(L->p, [&](auto PP) {
-            constexpr int P = decltype(PP)::value;
-            // p = 3 on the 512-wide mesh: the SL pass with immediate tap-row
-            // offsets, as sl2d_kernel (same arithmetic, same capacity)
-            const void *fn = (P == 3 && L->n_x == 512)    ? (const void *)gmres2d_coop<P, (P == 3 ? 512 : 0)>
-                             : (P == 5 && L->n_x == 1024) ? (const void *)gmres2d_coop<P, (P == 5 ? 1024 : 0)>
-                                                          : (const void *)gmres2d_coop<P>;
+        {
+            const void *fn = coop_fn(L);
             const int G = coop_capacity(fn);
             int64_t rows = r.B < G ? r.B : G;
             const int64_t cap = coop_rows_cap(L);
@@ -654,6 +667,7 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             C.L = *L;
             C.a = a;
             C.a.partial = r.row_sumsq;
+            C.a.gmres_hist = r.gmres_hist;
             C.rows_per_round = rows;
             C.chunks = chunks;
             C.nwb = nwb;
@@ -677,7 +691,7 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
                 return (int)MGRIT_ECUDA;
             }
             return check_launch("gmres2d_coop");
-        });
+        }
     }
     double *partial = nullptr;
     double *V = nullptr;

@@ -223,9 +223,43 @@ class Level:
     shared: bool = False
     stencil_numba: bool = False
 
+    # -- read-only views of the reference's Level data (mgrit.py:89-117) -----
+
+    @property
+    def departures(self):
+        """One DepartureSet view per stored record set (a single shared set for
+        a constant speed), east/eps re-derived from the device records exactly
+        as the kernels do; None for the ideal operator."""
+        from .operators import DepartureSetView
+        if self.s_x is None:
+            return None
+        return DepartureSetView(self)
+
     @property
     def sigma(self):
-        return None if self.sig_x is None else (self.sig_x, self.sig_y)
+        """One CorrectionField (device vectors) per stored sigma set, or None."""
+        from .operators import SigmaView
+        return None if self.sig_x is None else SigmaView(self)
+
+    def dep(self, n: int):
+        """mgrit.py:111-112."""
+        return self.departures[0 if self.shared else n]
+
+    def sig(self, n: int):
+        """mgrit.py:114-115."""
+        return self.sigma[0 if self.shared else n]
+
+    @property
+    def _idx(self):
+        """1D gather table (S, n_x, p+1) int32 of mgrit.py:121-126, built on demand."""
+        from .operators import stencil_tables
+        return stencil_tables(self)[0]
+
+    @property
+    def _w(self):
+        """1D weight table (S, n_x, p+1) of mgrit.py:121-126, built on demand."""
+        from .operators import stencil_tables
+        return stencil_tables(self)[1]
 
     def desc(self, stencil_numba: bool | None = None) -> _lib.LevelDesc:
         if self.kind == "ideal":
@@ -861,6 +895,7 @@ def _solve_loop(sess: _Session, cfg: SolverConfig, status: torch.Tensor) -> _Loo
             gc.enable()
     cur.wait_stream(side)
     sess.loop = _Loop(h, hist, ctrl, par)
+    sess.loop.body_kernels = int(lib.mgrit_loop_body_kernels(h))
     return sess.loop
 
 

@@ -1,0 +1,254 @@
+"""GPU parity of the exact kernel instantiations BASELINE configs 3-5 run in
+production, at their full mesh sizes (VERDICT r01 "What's weak" 1).
+
+* 2D SL step on config 5's 1024^2 mesh at p = 5: the FULL-tile sl2d_kernel,
+  bit-identical to the reference's tensor-product gather.
+* corrected steps through ``gmres2d_coop<5, 1024>`` (config 5, levels 1-2),
+  ``gmres2d_coop<3, 512>`` (config 4) and the generic instantiation on a
+  256^2 mesh (row-block addressing, many CTAs per system, several rounds of
+  systems per slot): rows within 1e-13 of the oracle, per-call GMRES counts
+  identical.
+* full-size solves against committed fixtures made by the real reference
+  (config 4; config 5's mesh for 128 steps) or by the bit-pinned oracle
+  (config 3, which the reference cannot hold in 62 GB): iteration counts,
+  status, residual histories within 1e-12 r0, and after every iteration the
+  iterate's row norms and 64 sampled columns within 1e-12 relative.
+
+The oracle is fed the DEVICE's departure records and sigma for the operator
+tests (their derivation is bit-pinned separately in test_gpu_parity.py), so
+no full-size oracle hierarchy has to be built on the GPU box's host.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2203_13382_b200 as P
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    return P
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _east_eps(s, n):
+    """decompose (semi_lagrangian.py:118-137) from the stored scaled coordinate."""
+    ef = np.ceil(s)
+    eps = ef - s
+    hi = eps >= 1.0
+    return np.mod(ef.astype(np.int64) - hi, n), np.where(hi, eps - 1.0, eps)
+
+
+def _oracle_level(lv, steps, gmres=(10, 1e-2)):
+    """An oracle OLevel whose records/sigma at ``steps`` are the device level's."""
+    n = lv.grid.n_x
+    deps = [None] * lv.n_steps
+    sig = [None] * lv.n_steps if lv.sig_x is not None else None
+    for t in steps:
+        ex, epx = _east_eps(_np(lv.s_x[t]), n)
+        ey, epy = _east_eps(_np(lv.s_y[t]), n)
+        deps[t] = O.Departures((ex, ey), (epx, epy), None, None)
+        if sig is not None:
+            sig[t] = (_np(lv.sig_x[t]), _np(lv.sig_y[t]))
+    kind = "fine" if lv.kind == "fine" else lv.kind
+    return O.OLevel(lv.index, 2, n, lv.p, lv.n_steps, lv.dt, kind, deps, sig, gmres=gmres)
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b.ravel())
+    return np.linalg.norm((a - b).ravel()) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def cfg5_mesh(P):
+    cfg = P.SolverConfig(n_x=1024, n_t=128, dim=2, wave_speed="B4", p=5, schedule=8, seed=4, u0="sin4")
+    return cfg, P.build_hierarchy(cfg)
+
+
+def test_sl2d_cfg5_mesh_p5_bitwise(P, cfg5_mesh):
+    """Config 5's fine SL step (1024^2, p = 5, FULL tiles) is bit-identical."""
+    _, levels = cfg5_mesh
+    fine = levels[0]
+    steps = [0, 37, 64, 127]
+    ol = _oracle_level(fine, steps)
+    U = np.random.default_rng(41).standard_normal((len(steps), fine.grid.n_points))
+    got = _np(fine.step_batch(np.array(steps), torch.from_numpy(U).cuda()))
+    for b, t in enumerate(steps):
+        assert np.array_equal(got[b], ol.step(t, U[b])), t
+
+
+def _corrected_rows(lv, steps, seed):
+    ol = _oracle_level(lv, steps)
+    log = O.GmresLog()
+    ol.log = log
+    U = np.random.default_rng(seed).standard_normal((len(steps), lv.grid.n_points))
+    want = np.stack([ol.step(t, U[b]) for b, t in enumerate(steps)])
+    iters = torch.zeros(len(steps), dtype=torch.int32, device="cuda")
+    out = torch.empty((len(steps), lv.grid.n_points), dtype=torch.float64, device="cuda")
+    lv._apply(torch.from_numpy(U).cuda(), 0, 0, len(steps), out,
+              t_idx=torch.as_tensor(steps, device="cuda"), gmres_iters=iters)
+    got = _np(out)
+    for b in range(len(steps)):
+        assert _rel(got[b], want[b]) < 1e-13, (lv.index, steps[b], _rel(got[b], want[b]))
+    assert list(_np(iters)) == log.counts, (list(_np(iters)), log.counts)
+    return log.counts
+
+
+@pytest.mark.parametrize("li,steps", [(1, [0, 5, 9, 15]), (2, [0, 1])])
+def test_corrected_cfg5_mesh_gmres2d_coop_5_1024(P, cfg5_mesh, li, steps):
+    """Config 5's corrected levels: gmres2d_coop<5, 1024> with 2 systems in
+    flight per round (L2-sized) over ~296 CTAs each; 4 rows = 2 rounds."""
+    _, levels = cfg5_mesh
+    counts = _corrected_rows(levels[li], steps, seed=li)
+    assert all(c >= 1 for c in counts)
+
+
+@pytest.fixture(scope="module")
+def cfg4_mesh(P):
+    cfg = P.SolverConfig(n_x=512, n_t=64, dim=2, wave_speed="B4", p=3, schedule=4, seed=3, u0="sin4")
+    return cfg, P.build_hierarchy(cfg)
+
+
+@pytest.mark.parametrize("li,steps", [(1, [0, 3, 7, 8, 12, 15]), (2, [0, 1, 2, 3])])
+def test_corrected_cfg4_mesh_gmres2d_coop_3_512(P, cfg4_mesh, li, steps):
+    """Config 4's corrected levels through gmres2d_coop<3, 512>."""
+    _, levels = cfg4_mesh
+    _corrected_rows(levels[li], steps, seed=10 + li)
+
+
+@pytest.mark.parametrize("p", [3, 5])
+def test_corrected_256_mesh_row_blocks_multichunk(P, p):
+    """The generic instantiation on a 256^2 mesh: row-block addressing
+    (n_x % 256 == 0), every system split over many CTAs that all hold data,
+    and more systems than slots."""
+    cfg = P.SolverConfig(n_x=256, n_t=64, dim=2, wave_speed="B4", p=p, schedule=4, seed=3)
+    levels = P.build_hierarchy(cfg)
+    _corrected_rows(levels[1], list(range(16)), seed=p)
+
+
+@pytest.mark.parametrize("mode", ["fixed", "tolerance"])
+def test_corrected_cfg5_mesh_fixed_and_tol(P, mode):
+    """Both GMRES modes at 1024^2 (fixed K = 10 runs every Arnoldi step)."""
+    cfg = P.SolverConfig(n_x=1024, n_t=16, dim=2, wave_speed="B4", p=5, schedule=8, seed=4, gmres_mode=mode)
+    levels = P.build_hierarchy(cfg)
+    lv = levels[1]
+    steps = [0, 1]
+    ol = _oracle_level(lv, steps, gmres=(10, None if mode == "fixed" else 1e-2))
+    log = O.GmresLog()
+    ol.log = log
+    U = np.random.default_rng(7).standard_normal((2, lv.grid.n_points))
+    want = np.stack([ol.step(t, U[b]) for b, t in enumerate(steps)])
+    iters = torch.zeros(2, dtype=torch.int32, device="cuda")
+    out = torch.empty((2, lv.grid.n_points), dtype=torch.float64, device="cuda")
+    lv._apply(torch.from_numpy(U).cuda(), 0, 0, 2, out, t_idx=torch.as_tensor(steps, device="cuda"),
+              gmres_iters=iters)
+    assert _rel(_np(out), want) < 1e-13
+    assert list(_np(iters)) == log.counts
+
+
+# ---------------------------------------------------------------------------
+# full-size solves against committed fixtures
+
+
+def _fixture(name):
+    path = os.path.join(GOLDEN, f"solve_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"fixture {name} not generated")
+    g = dict(np.load(path))
+    g["meta"] = json.loads(str(g["meta"]))
+    return g
+
+
+FULLSIZE = {
+    "cfg4_full": None,           # whole solve if the fixture converged
+    "cfg5mesh_nt128": None,
+    "cfg3_full": None,
+}
+
+
+def _oracle_fine_coords(kw):
+    """The reference's (numpy) ERK departure coordinates of every fine step
+    (erk_departures at t = n dt, semi_lagrangian.py:75-115, 208-217)."""
+    ocfg = O.OConfig(**kw)
+    dim, n_x = ocfg.dim, ocfg.n_x
+    dt = ocfg.dt if ocfg.dt is not None else 0.85 * 2.0 / n_x
+    arr = O.nodes(dim, n_x)
+    n = n_x ** dim
+    if dim == 1:
+        C = np.empty((ocfg.n_t, n))
+        for k in range(ocfg.n_t):
+            C[k] = O.erk_trace(ocfg.wave_speed, arr, k * dt, dt, ocfg.order)
+        return C
+    CX, CY = np.empty((ocfg.n_t, n)), np.empty((ocfg.n_t, n))
+    for k in range(ocfg.n_t):
+        CX[k], CY[k] = O.erk_trace(ocfg.wave_speed, arr, k * dt, dt, ocfg.order)
+    return CX, CY
+
+
+def _check_fullsize(P, g, levels, it_tol):
+    meta = g["meta"]
+    kw = dict(meta["kw"])
+    k = meta["iterations"]
+    hist = g["hist"]
+    r0 = hist[0]
+    converged = meta["status"] == "converged"
+    cfg = P.SolverConfig(**kw) if converged else P.SolverConfig(**{**kw, "max_iters": k, "rtol": 0.0})
+    assert [lv.n_steps for lv in levels] == meta["levels"]
+    rep, U = P.solve(cfg, levels, output="device")
+    if converged:
+        assert rep.status == "converged" and rep.iterations == k, (rep.status, rep.iterations, k)
+    assert len(rep.residual_norms) == len(hist)
+    dev = np.abs(rep.residual_norms - hist) / r0
+    assert np.all(dev <= 1e-12), dev.max()
+    # the iterate after every iteration: row norms and the sampled columns
+    idx = torch.as_tensor(g["cols_idx"], device="cuda")
+    worst = 0.0
+    for j in range(1, k + 1):
+        if j < k:
+            _, Uj = P.solve(P.SolverConfig(**{**kw, "max_iters": j, "rtol": 0.0}), levels, output="device")
+        else:
+            Uj = U
+        norms = _np(torch.linalg.vector_norm(Uj, dim=1))
+        cols = _np(Uj[:, idx])
+        rel_n = float(np.max(np.abs(norms - g["row_norms"][j - 1]) / np.maximum(g["row_norms"][j - 1], 1e-300)))
+        rel_c = _rel(cols, g["cols"][j - 1])
+        worst = max(worst, rel_n, rel_c)
+        assert rel_n <= it_tol and rel_c <= it_tol, (j, rel_n, rel_c)
+    return worst
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", sorted(FULLSIZE))
+def test_fullsize_parity_mode_matches_fixture(P, name):
+    """Fed the reference's own (numpy) ERK departure coordinates, the full-size
+    solve reproduces the fixture: count/status, history within 1e-12 r0, and
+    the iterate after EVERY iteration within relative 1e-12 (north_star)."""
+    g = _fixture(name)
+    kw = dict(g["meta"]["kw"])
+    levels = P.build_hierarchy(P.SolverConfig(**kw), fine_coords=_oracle_fine_coords(kw))
+    _check_fullsize(P, g, levels, 1e-12)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", sorted(FULLSIZE))
+def test_fullsize_product_mode_matches_fixture(P, name):
+    """The product path (departures traced on the device: CUDA sin/cos are
+    ulps away from numpy's) gives the same counts/status and histories within
+    1e-12 r0; its iterates carry the traced-departure ulps amplified over
+    thousands of steps and stay within 1e-11 relative."""
+    g = _fixture(name)
+    kw = dict(g["meta"]["kw"])
+    levels = P.build_hierarchy(P.SolverConfig(**kw))
+    _check_fullsize(P, g, levels, 1e-11)
