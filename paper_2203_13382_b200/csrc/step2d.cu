@@ -228,6 +228,120 @@ __global__ void __launch_bounds__(kNT2, MINB) sl2d_kernel(mgrit_level_desc L, Ro
     }
 }
 
+// Column-strip SL step: each thread owns NB vertically adjacent nodes of one
+// column (a CTA: 256 columns x NB grid rows, warps coalesced along x).
+// Where the strip's x-records are bitwise equal (the x-departure does not
+// depend on y, e.g. BASELINE's speed (cos^2(pi x)cos(2 pi t) + 0.5, ...))
+// and its y-departure rows are consecutive, every node's x-interpolation of
+// an absolute source row is the SAME rounded value: the strip computes the
+// NB + P row sums once (x-weights once, each tap loaded once) and every node
+// combines P + 1 of them with its own y-weights.  The arithmetic of each node
+// is exactly the reference's (x inner from 0, y outer from 0, separately
+// rounded), so the result is bit-identical; only identical subexpressions
+// are shared.  Strips that do not qualify take the per-node path.
+// Per node-update at p = 5, NB = 4: ~110 FP64 instructions and ~15 loads
+// instead of 185 and 38.
+template <int P, int NB, bool SLONLY, int NX = 0>
+__global__ void __launch_bounds__(kNT2, 4) sl2d_strip_kernel(mgrit_level_desc L, Rows2D a) {
+    __shared__ double red[kNT2 / 32 + 1];
+    constexpr int SL = Stencil<P>::L, R = Stencil<P>::R;
+    const int nx = NX > 0 ? NX : L.n_x;
+    const int64_t n = (int64_t)nx * nx;
+    const int tiles_x = nx / kNT2;
+    const int band = blockIdx.x / tiles_x;
+    const int ix = (blockIdx.x - band * tiles_x) * kNT2 + threadIdx.x;
+    const int iy0 = band * NB;
+    const int64_t b = blockIdx.y;
+    const int64_t t = row_t(a, b);
+    const int64_t set = L.shared ? 0 : t;
+    const double *sxp = L.s_x + set * n, *syp = L.s_y + set * n;
+    const double *u = a.U_in + b * a.ld_in;
+    double sx[NB], sy[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int64_t i = (int64_t)(iy0 + k) * nx + ix;
+        sx[k] = __ldcs(sxp + i);
+        sy[k] = __ldcs(syp + i);
+    }
+    bool same = true;
+#pragma unroll
+    for (int k = 1; k < NB; ++k) same = same && (__double_as_longlong(sx[k]) == __double_as_longlong(sx[0]));
+    const Dec dx = decompose_s(sx[0], nx);
+    const Dec dy0 = decompose_s(sy[0], nx);
+    bool fast = same && dx.e >= SL && dx.e + R < nx;
+    double out[NB];
+    if (fast) {
+        // consecutive y-departure rows (no wrap inside the check: row indices mod n)
+#pragma unroll
+        for (int k = 1; k < NB; ++k) {
+            int want = dy0.e + k;
+            if (want >= nx) want -= nx;
+            fast = fast && decompose_s(sy[k], nx).e == want;
+        }
+    }
+    if (fast) {
+        double wx[P + 1];
+        lagrange_weights<P>(dx.eps, wx);
+        double acc[NB + P];
+#pragma unroll
+        for (int r = 0; r < NB + P; ++r) {
+            int row = dy0.e - SL + r;
+            row = row < 0 ? row + nx : (row >= nx ? row - nx : row);
+            const double *src = u + (int64_t)row * nx + (dx.e - SL);
+            double s = 0.0;
+#pragma unroll
+            for (int jx = 0; jx <= P; ++jx) s = __dadd_rn(s, __dmul_rn(wx[jx], __ldg(src + jx)));
+            acc[r] = s;
+        }
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+            const Dec dy = decompose_s(sy[k], nx);
+            double wy[P + 1];
+            lagrange_weights<P>(dy.eps, wy);
+            double o = 0.0;
+#pragma unroll
+            for (int jy = 0; jy <= P; ++jy) o = __dadd_rn(o, __dmul_rn(wy[jy], acc[k + jy]));
+            out[k] = o;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) out[k] = sl2d_at<P, NX>(u, nx, sx[k], sy[k]);
+    }
+    double ss = 0.0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int64_t i = (int64_t)(iy0 + k) * nx + ix;
+        double v = out[k];
+        if constexpr (!SLONLY) {
+            const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
+            if (a.U_sub) {
+                v = __dsub_rn(__dadd_rn(g, v), a.U_sub[b * a.ld_sub + i]);
+            } else {
+                v = __dadd_rn(v, g);
+            }
+            ss = __dadd_rn(ss, __dmul_rn(v, v));
+        }
+        if (a.out) a.out[b * a.ld_out + i] = v;
+    }
+    if constexpr (!SLONLY) {
+        if (a.partial) {
+            const double tot = block_sum<kNT2>(ss, red);
+            if (threadIdx.x == 0) a.partial[b * gridDim.x + blockIdx.x] = tot;
+        }
+    }
+}
+
+// strip height of sl2d_strip_kernel (MGRIT_SL2D_STRIP overrides; 0 = off)
+static int strip_rows() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MGRIT_SL2D_STRIP");
+        v = e ? atoi(e) : 4;
+        if (v != 0 && v != 2 && v != 4 && v != 8) v = 4;
+    }
+    return v;
+}
+
 // forward Euler finish: out = (2 v - imsd(v)) [+ G | residual form], v from scratch
 template <int P>
 __global__ void __launch_bounds__(kNT2) fe2d_kernel(mgrit_level_desc L, Rows2D a, const double *V) {
@@ -626,7 +740,27 @@ int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows) {
     }
     // FE needs the SL rows; all kinds need tile partials for row norms
     const int64_t r = rows < 1 ? 1 : rows;
-    return (L->kind == MGRIT_KIND_FORWARD_EULER ? 8 * r * n : 0) + 8 * r * tiles_for(n) + 256;
+    // partials: one per 1024-node tile, or per 512-node strip tile (NB = 2)
+    return (L->kind == MGRIT_KIND_FORWARD_EULER ? 8 * r * n : 0) + 2 * 8 * r * tiles_for(n) + 256;
+}
+
+template <int P, bool SO>
+static void launch_strip(int nb, dim3 g, const mgrit_level_desc *L, const Rows2D &s, cudaStream_t st) {
+    auto go = [&](auto NBC) {
+        constexpr int NB = decltype(NBC)::value;
+        if (P == 5 && L->n_x == 1024)
+            sl2d_strip_kernel<P, NB, SO, (P == 5 ? 1024 : 0)><<<g, kNT2, 0, st>>>(*L, s);
+        else if (P == 3 && L->n_x == 512)
+            sl2d_strip_kernel<P, NB, SO, (P == 3 ? 512 : 0)><<<g, kNT2, 0, st>>>(*L, s);
+        else
+            sl2d_strip_kernel<P, NB, SO, 0><<<g, kNT2, 0, st>>>(*L, s);
+    };
+    if (nb == 2)
+        go(std::integral_constant<int, 2>{});
+    else if (nb == 8)
+        go(std::integral_constant<int, 8>{});
+    else
+        go(std::integral_constant<int, 4>{});
 }
 
 static int validate2d(const mgrit_level_desc *L) {
@@ -700,36 +834,49 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
         scr += 8 * r.B * n;
     }
     if (r.row_sumsq) partial = (double *)scr;
-    const int64_t need = (V ? 8 * r.B * n : 0) + (partial ? 8 * r.B * tiles : 0);
+    // column-strip form on meshes whose width is a multiple of the 256-column
+    // CTA (every BASELINE 2D mesh); the per-node kernel elsewhere
+    const int nb = strip_rows();
+    const bool strip = nb > 0 && L->n_x % kNT2 == 0 && L->n_x % nb == 0;
+    const int64_t ptiles = strip ? n / ((int64_t)kNT2 * nb) : tiles;
+    const int64_t need = (V ? 8 * r.B * n : 0) + (partial ? 8 * r.B * ptiles : 0);
     if (need > scratch_bytes) return MGRIT_EINVAL;
     const dim3 grid((unsigned)tiles, (unsigned)r.B);
+    const dim3 sgrid((unsigned)ptiles, (unsigned)r.B);
     return dispatch_p(L->p, [&](auto PP) {
         constexpr int P = decltype(PP)::value;
         if (L->kind == MGRIT_KIND_FORWARD_EULER) {
             Rows2D s = a;
             s.out = V;
             s.ld_out = n;
-            if (P == 5 && n % kTile2 == 0)
+            if (strip)
+                launch_strip<P, true>(nb, sgrid, L, s, st);
+            else if (P == 5 && n % kTile2 == 0)
                 sl2d_kernel<P, true, SL2DMinBlocks<P>::value, true, P == 5><<<grid, kNT2, 0, st>>>(*L, s);
             else
                 sl2d_kernel<P, true, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
             Rows2D f = a;
             f.partial = partial;
             fe2d_kernel<P><<<grid, kNT2, 0, st>>>(*L, f, V);
-        } else {
-            Rows2D s = a;
-            s.partial = partial;
+            if (partial) rowsum_kernel<<<(unsigned)(r.B < 4096 ? r.B : 4096), kNT2, 0, st>>>(partial, tiles, r.B, r.row_sumsq);
+            return check_launch("apply_rows_2d");
+        }
+        Rows2D s = a;
+        s.partial = partial;
+        if (strip) {
+            launch_strip<P, false>(nb, sgrid, L, s, st);
+        } else if (P == 3 && L->n_x == 512) {
             // p = 3 on the 512-wide mesh (cfg4): the tap rows are immediate
             // offsets from one base pointer (0.676 -> 0.618 ms per F-step);
             // at p = 5 the same form measured slower (4.69 -> 4.91 ms)
-            if (P == 3 && L->n_x == 512)
-                sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true, false, 512><<<grid, kNT2, 0, st>>>(*L, s);
-            else if (P == 5 && n % kTile2 == 0)
-                sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true, P == 5><<<grid, kNT2, 0, st>>>(*L, s);
-            else
-                sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
+            sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true, false, 512><<<grid, kNT2, 0, st>>>(*L, s);
+        } else if (P == 5 && n % kTile2 == 0) {
+            sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true, P == 5><<<grid, kNT2, 0, st>>>(*L, s);
+        } else {
+            sl2d_kernel<P, false, SL2DMinBlocks<P>::value, true><<<grid, kNT2, 0, st>>>(*L, s);
         }
-        if (partial) rowsum_kernel<<<(unsigned)(r.B < 4096 ? r.B : 4096), kNT2, 0, st>>>(partial, tiles, r.B, r.row_sumsq);
+        if (partial)
+            rowsum_kernel<<<(unsigned)(r.B < 4096 ? r.B : 4096), kNT2, 0, st>>>(partial, (int)ptiles, r.B, r.row_sumsq);
         return check_launch("apply_rows_2d");
     });
 }

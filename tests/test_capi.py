@@ -163,22 +163,20 @@ def test_product_fails_loudly_without_cuda():
 
 
 def test_cli_parse_and_config(tmp_path):
+    """Config file + explicit flags (flags win), per-level schedules, bad input
+    -> ValueError / exit status 2 (reference cli.py:93-125 behaviour)."""
     from paper_2203_13382_b200 import cli
-    assert cli.parse_size("(2^6)^2x2^10") == 2 ** 22
-    with pytest.raises(ValueError):
-        cli.parse_size("2^x")
     cfgf = tmp_path / "c.json"
     cfgf.write_text('{"n_x": 64, "n_t": 128, "p": 3, "wave_speed": "C3"}')
-    parser = cli.build_parser()
-    argv = ["run", "--config", str(cfgf), "-p", "5"]
-    args = parser.parse_args(argv)
-    args.explicit = cli._explicit_dests(parser._run_parser, argv)
-    cfg = cli.config_from_namespace(args)
+    cfg = cli.make_config({"p": 5}, str(cfgf))
     assert (cfg.n_x, cfg.n_t, cfg.p, cfg.wave_speed) == (64, 128, 5, "C3")
+    assert cli.make_config({"n_x": 8, "n_t": 64, "schedule": "16,4"}, None).schedule == [16, 4]
+    assert cli.make_config({"n_x": 8, "n_t": 64, "schedule": "8"}, None).schedule == 8
     bad = tmp_path / "b.json"
     bad.write_text('{"n_x": 64, "n_t": 128, "bogus": 1}')
-    args = parser.parse_args(["run", "--config", str(bad)])
-    args.explicit = set()
     with pytest.raises(ValueError):
-        cli.config_from_namespace(args)
+        cli.make_config({}, str(bad))
+    with pytest.raises(ValueError):
+        cli.make_config({"n_x": 64}, None)
     assert cli.main(["run", "--config", str(bad)]) == 2
+    assert cli.main(["run", "--nx", "64"]) == 2

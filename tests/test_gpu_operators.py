@@ -17,6 +17,7 @@ import pytest
 import torch
 
 import oracle as O
+from oracle import mgrit_oracle as OM
 
 pytestmark = pytest.mark.gpu
 
@@ -96,8 +97,10 @@ def test_gmres_solve_matches_reference(P, ops, dim, n, p, scale, mode):
     cfg = P.GmresConfig(10, None if mode == "fixed" else 1e-2)
     x, hist = P.gmres_solve(op, ops[key + "_rhs"], cfg)
     want_x, want_h = ops[key + f"_{mode}_x"], ops[key + f"_{mode}_hist"]
-    assert len(hist) == len(want_h)
-    assert np.allclose(hist, want_h, rtol=1e-12, atol=1e-300)
+    assert len(hist) == len(want_h)                      # the iteration count
+    # |g_k| differences relative to beta (the solve-history bar: late entries
+    # are tiny and carry the reductions' rounding relative to beta, not to themselves)
+    assert np.max(np.abs(hist - want_h)) <= 1e-12 * want_h[0]
     assert np.linalg.norm(x - want_x) <= 1e-13 * max(np.linalg.norm(want_x), 1e-300)
 
 
@@ -135,7 +138,7 @@ def test_coarse_steps_match_oracle(P, dim, n, speed, p):
         want, _ = O.gmres(lambda v: O.imsd(sig, O.d_stencil(p), v, n), O.sl_apply(dim, n, p, od, u), 10, tol)
         assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
     fe = P.forward_euler_coarse_step(grid, dep, p, field, u)
-    assert np.array_equal(fe, O.ipsd(sig, O.d_stencil(p), O.sl_apply(dim, n, p, od, u), n))
+    assert np.array_equal(fe, OM.ipsd(sig, O.d_stencil(p), O.sl_apply(dim, n, p, od, u), n))
 
 
 def test_level_views_match_oracle_records(P):
@@ -159,7 +162,7 @@ def test_level_views_match_oracle_records(P):
                 if ol.sigma is not None:
                     assert np.array_equal(_np(lv.sig(n).x), ol.sig(n)[0])
             if lv.grid.dim == 1:
-                ell, r = O.extents(lv.p)
+                ell, r = OM.extents(lv.p)
                 want_idx = np.stack([np.stack([np.mod(d.east[0] + j, lv.grid.n_x) for j in range(-ell, r + 1)], 1)
                                      for d in ol.deps])
                 assert np.array_equal(_np(lv._idx), want_idx)
