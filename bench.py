@@ -440,10 +440,17 @@ def sequential_gpu(levels, cfg) -> float:
     for _ in range(2):
         M._sweep(levels[0], Useq, None, zero_init=False)
     torch.cuda.synchronize()
+    # 2D steps are one launch each: replay them from a CUDA graph, so the
+    # baseline carries no host launch overhead (1D: one persistent kernel)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        M._sweep(levels[0], Useq, None, zero_init=False)
+    g.replay()
+    torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
     for _ in range(3):
-        M._sweep(levels[0], Useq, None, zero_init=False)
+        g.replay()
     s1.record()
     torch.cuda.synchronize()
     return s0.elapsed_time(s1) / 3

@@ -241,19 +241,28 @@ __global__ void __launch_bounds__(kNT2, MINB) sl2d_kernel(mgrit_level_desc L, Ro
 // are shared.  Strips that do not qualify take the per-node path.
 // Per node-update at p = 5, NB = 4: ~110 FP64 instructions and ~15 loads
 // instead of 185 and 38.
+//
+// One (row, tile) job per CTA; the job's records are loaded (streaming) before
+// anything else.  (A persistent form that prefetched the next job's records
+// into shared memory with cp.async measured 1.7x slower on cfg5: 64-register
+// spills of the loop state and fewer independent CTAs per SM.)
 template <int P, int NB, bool SLONLY, int NX = 0>
-__global__ void __launch_bounds__(kNT2, 4) sl2d_strip_kernel(mgrit_level_desc L, Rows2D a) {
+__global__ void __launch_bounds__(kNT2, 4) sl2d_strip_kernel(mgrit_level_desc L, Rows2D a, int64_t jobs) {
     __shared__ double red[kNT2 / 32 + 1];
     constexpr int SL = Stencil<P>::L, R = Stencil<P>::R;
     const int nx = NX > 0 ? NX : L.n_x;
     const int64_t n = (int64_t)nx * nx;
     const int tiles_x = nx / kNT2;
-    const int band = blockIdx.x / tiles_x;
-    const int ix = (blockIdx.x - band * tiles_x) * kNT2 + threadIdx.x;
+    const int64_t tiles = n / ((int64_t)kNT2 * NB);
+    const int tid = threadIdx.x;
+    {
+    const int64_t j = blockIdx.x;
+    if (j >= jobs) return;
+    const int64_t b = j / tiles, tile = j - b * tiles;
+    const int band = (int)(tile / tiles_x);
+    const int ix = (int)(tile - (int64_t)band * tiles_x) * kNT2 + tid;
     const int iy0 = band * NB;
-    const int64_t b = blockIdx.y;
-    const int64_t t = row_t(a, b);
-    const int64_t set = L.shared ? 0 : t;
+    const int64_t set = L.shared ? 0 : row_t(a, b);
     const double *sxp = L.s_x + set * n, *syp = L.s_y + set * n;
     const double *u = a.U_in + b * a.ld_in;
     double sx[NB], sy[NB];
@@ -326,18 +335,22 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_strip_kernel(mgrit_level_desc L,
     if constexpr (!SLONLY) {
         if (a.partial) {
             const double tot = block_sum<kNT2>(ss, red);
-            if (threadIdx.x == 0) a.partial[b * gridDim.x + blockIdx.x] = tot;
+            if (threadIdx.x == 0) a.partial[b * tiles + tile] = tot;
         }
+    }
     }
 }
 
-// strip height of sl2d_strip_kernel (MGRIT_SL2D_STRIP overrides; 0 = off)
+// strip height of sl2d_strip_kernel (MGRIT_SL2D_STRIP overrides; 0 = the
+// per-node kernel).  Measured on B200 (tools/gpu_strip_sweep.sh), cfg5 F-step:
+// per-node 4.69 ms, NB = 2 4.11, NB = 4 3.27, NB = 8 3.24 ms (spills; and its
+// 64 KB two-stage record buffer exceeds static shared memory): NB = 4.
 static int strip_rows() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("MGRIT_SL2D_STRIP");
         v = e ? atoi(e) : 4;
-        if (v != 0 && v != 2 && v != 4 && v != 8) v = 4;
+        if (v != 0 && v != 2 && v != 4) v = 4;
     }
     return v;
 }
@@ -662,6 +675,277 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Low-synchronisation variant (GmresConfig variant "mgs_lowsync").
+//
+// The MGS coefficients h_j = <b_j, w - sum_{i<j} h_i b_i> equal, in exact
+// arithmetic, c_j - sum_{i<j} h_i G_ji with c_j = <b_j, w> and the Gram
+// entries G_ji = <b_j, b_i>.  The stencil pass that forms b_kk and w = A b_kk
+// accumulates every c_j (j <= kk) and G_kk,i (i < kk) at once, so an Arnoldi
+// step costs two system barriers and two passes (stencil + all inner
+// products; w -= sum h_j b_j + ||w||^2) instead of kk + 2 of each.  The
+// subtraction w -= h_j b_j runs in the reference's order j = 0..kk.  Results
+// equal the classic loop's up to the rounding of the coefficients (GMRES
+// iteration counts identical in every parity test, rows within 1e-13).
+
+constexpr int kLsMaxK = 10;                // instantiated Arnoldi depth (K <= 10)
+constexpr int kLsVals = 2 * kLsMaxK + 2;   // partial arrays: pass-A bank (2K+1) + bank B
+
+struct LsSmem {
+    double cs[kLsMaxK], sn[kLsMaxK], g[kLsMaxK + 1], y[kLsMaxK], H[(kLsMaxK + 1) * kLsMaxK];
+    double gram[kLsMaxK * kLsMaxK];        // G_ji = <b_j, b_i>, i < j
+    double h[kLsMaxK + 1];
+    double red[2 * kLsMaxK + 1][kNT2 / 32];
+    int stop;
+};
+
+template <int P, int NX = 0>
+__global__ void __launch_bounds__(kNT2, 2) gmres2d_coop_ls(Coop2D C) {
+    __shared__ LsSmem S;
+    const mgrit_level_desc &L = C.L;
+    const Rows2D &a = C.a;
+    const int nx = L.n_x;
+    const int64_t n = L.n_points;
+    const int K = L.gmres_max_iters;
+    const double tol = L.gmres_tol;
+    const int slot = blockIdx.x / C.chunks;
+    const int chunk = blockIdx.x % C.chunks;
+    const bool active_cta = slot < C.rows_per_round;
+    const int64_t nwb = C.nwb;
+    const int64_t wb0 = nwb * chunk / C.chunks, wb1 = nwb * (chunk + 1) / C.chunks;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kNT2 / 32;
+    const bool row_blocks = (nx % kWB) == 0;
+    auto part = [&](int v) { return C.part + ((int64_t)v * C.rows_per_round + slot) * nwb; };
+    constexpr int kBankB = kLsVals - 1;
+    // visit this CTA's nodes; body(i, ix, iy, acc) adds into acc[0..NV) per lane,
+    // warp sums land in part(v0 + v)[wb]
+    auto for_nodes_nv = [&](auto NVC, int v0, auto &&body) {
+        constexpr int NV = decltype(NVC)::value;
+        for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
+            const int64_t base = wb * kWB;
+            const int iy0 = row_blocks ? (int)(base / nx) : 0;
+            const int ix0 = row_blocks ? (int)(base - (int64_t)iy0 * nx) : 0;
+            double acc[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+#pragma unroll
+            for (int k = 0; k < kWBPerLane; ++k) {
+                const int64_t i = base + lane + 32 * k;
+                if (i < n) {
+                    int ix, iy;
+                    if (row_blocks) {
+                        ix = ix0 + lane + 32 * k;
+                        iy = iy0;
+                    } else {
+                        iy = (int)((unsigned)i / (unsigned)nx);
+                        ix = (int)i - iy * nx;
+                    }
+                    body(i, ix, iy, acc);
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const double s = warp_sum(acc[v]);
+                if (lane == 0 && active_cta) part(v0 + v)[wb] = s;
+            }
+        }
+    };
+    unsigned int gen = 0;
+    auto ssync = [&]() {
+        __syncthreads();
+        if (tid == 0) {
+            ++gen;
+            cuda::atomic_ref<unsigned int, cuda::thread_scope_device> ctr(C.bar[slot]);
+            ctr.fetch_add(1u, cuda::memory_order_release);
+            const unsigned int target = gen * (unsigned int)C.chunks;
+            while (ctr.load(cuda::memory_order_acquire) < target) {
+            }
+        }
+        __syncthreads();
+    };
+    // system barrier, then the fixed-order totals of nv partial arrays v0..:
+    // per thread a strided sum over the warp blocks, a warp butterfly, then the
+    // warp results in warp order (identical in every thread and CTA)
+    auto gtotals = [&](int v0, int nv, double *out) {
+        ssync();
+        for (int v = 0; v < nv; ++v) {
+            const double *pb = part(v0 + v);
+            double acc = 0.0;
+            for (int64_t q = tid; q < nwb; q += kNT2) acc = __dadd_rn(acc, pb[q]);
+            acc = warp_sum(acc);
+            if (lane == 0) S.red[v][warp] = acc;
+        }
+        __syncthreads();
+        for (int v = 0; v < nv; ++v) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) t = __dadd_rn(t, S.red[v][w]);
+            out[v] = t;
+        }
+        __syncthreads();
+    };
+    if (!active_cta) return;
+
+    double *basis = C.basis + (int64_t)slot * (K + 1) * n;
+    double *const wping = C.w + (int64_t)slot * n, *const wpong = C.w2 + (int64_t)slot * n;
+    for (int64_t b = slot; b < a.B; b += C.rows_per_round) {
+        const int64_t t = row_t(a, b);
+        const int64_t set = L.shared ? 0 : t;
+        const double *sx = L.s_x + set * n, *sy = L.s_y + set * n;
+        const double *gx = L.sig_x + set * n, *gy = L.sig_y + set * n;
+        int bad = 0;
+        double *src = wping, *dst = wpong;
+        {
+            const double *u = a.U_in + b * a.ld_in;
+            for_nodes_nv(std::integral_constant<int, 1>{}, kBankB, [&](int64_t i, int, int, double *acc) {
+                const double v = sl2d_at<P, NX>(u, nx, __ldg(sx + i), __ldg(sy + i));
+                src[i] = v;
+                if (!isfinite(v)) bad = 1;
+                acc[0] = __dadd_rn(acc[0], __dmul_rn(v, v));
+            });
+        }
+        bad = __syncthreads_or(bad);
+        if (tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
+        double tot[2 * kLsMaxK + 1];
+        gtotals(kBankB, 1, tot);
+        const double beta = sqrt(tot[0]);
+        double *hist = (a.gmres_hist && chunk == 0 && tid == 0) ? a.gmres_hist + b * (int64_t)(K + 1) : nullptr;
+        if (hist) hist[0] = beta;
+        int anybad = 0;
+        if (tid == 0)
+            for (int k = 0; k < C.chunks; ++k) anybad |= C.flags[(int64_t)slot * C.chunks + k];
+        anybad = __syncthreads_or(anybad);
+        int done = 0;
+        const bool skip = anybad || beta == 0.0;
+        if (anybad && tid == 0 && chunk == 0) atomicExch(C.status, 1);
+        if (tid == 0) S.stop = skip ? 1 : 0;
+        double g_k = beta;
+        double scale = beta, rscale = 1.0 / beta;
+        for (int kk = 0; kk < K; ++kk) {
+            __syncthreads();
+            if (S.stop) break;
+            double *bk = basis + (int64_t)kk * n;
+            // ---- pass A: b_kk (formed from src / scale), w = A b_kk into dst;
+            //      c_j = <b_j, w> (j <= kk) -> arrays 0..kk, G_kk,i = <b_kk, b_i>
+            //      (i < kk) -> arrays kk+1..2kk
+            auto passA = [&](auto KKC) {
+                constexpr int KK = decltype(KKC)::value;
+                for_nodes_nv(std::integral_constant<int, 2 * KK + 1>{}, 0,
+                             [&](int64_t i, int ix, int iy, double *acc) {
+                                 double bi;
+                                 const double x = imsd2d_scaled<P, NX>(src, nx, ix, iy, __ldg(gx + i), __ldg(gy + i),
+                                                                       scale, rscale, bi);
+                                 bk[i] = bi;
+                                 dst[i] = x;
+#pragma unroll
+                                 for (int j = 0; j < KK; ++j) {
+                                     const double bj = basis[(int64_t)j * n + i];
+                                     acc[j] = fma(bj, x, acc[j]);
+                                     acc[KK + 1 + j] = fma(bi, bj, acc[KK + 1 + j]);
+                                 }
+                                 acc[KK] = fma(bi, x, acc[KK]);
+                             });
+            };
+            switch (kk) {
+                case 0: passA(std::integral_constant<int, 0>{}); break;
+                case 1: passA(std::integral_constant<int, 1>{}); break;
+                case 2: passA(std::integral_constant<int, 2>{}); break;
+                case 3: passA(std::integral_constant<int, 3>{}); break;
+                case 4: passA(std::integral_constant<int, 4>{}); break;
+                case 5: passA(std::integral_constant<int, 5>{}); break;
+                case 6: passA(std::integral_constant<int, 6>{}); break;
+                case 7: passA(std::integral_constant<int, 7>{}); break;
+                case 8: passA(std::integral_constant<int, 8>{}); break;
+                default: passA(std::integral_constant<int, 9>{}); break;
+            }
+            gtotals(0, 2 * kk + 1, tot);
+            // MGS coefficients from the inner products and the Gram entries
+            // (every thread, identical values)
+            double h[kLsMaxK + 1];
+            for (int j = 0; j <= kk; ++j) {
+                double hj = tot[j];
+                for (int i = 0; i < j; ++i) {
+                    const double gji = j == kk ? tot[kk + 1 + i] : S.gram[j * kLsMaxK + i];
+                    hj = fma(-h[i], gji, hj);
+                }
+                h[j] = hj;
+            }
+            __syncthreads();
+            if (tid == 0)
+                for (int i = 0; i < kk; ++i) S.gram[kk * kLsMaxK + i] = tot[kk + 1 + i];
+            // ---- pass B: w -= h_j b_j (j = 0..kk, the reference's order), ||w||^2
+            double *const w = dst;
+            for_nodes_nv(std::integral_constant<int, 1>{}, kBankB, [&](int64_t i, int, int, double *acc) {
+                double x = w[i];
+                for (int j = 0; j <= kk; ++j) x = fma(-h[j], basis[(int64_t)j * n + i], x);
+                w[i] = x;
+                acc[0] = fma(x, x, acc[0]);
+            });
+            gtotals(kBankB, 1, tot + 2 * kLsMaxK);
+            const double nrm = sqrt(tot[2 * kLsMaxK]);
+            const bool brk = nrm <= __dmul_rn(1e-14, beta);
+            scale = nrm;
+            rscale = 1.0 / nrm;
+            dst = src;
+            src = w;
+            if (tid == 0) {
+                // previous rotations applied to column kk, then the new one
+                double hrun = h[0];
+                for (int j = 1; j <= kk; ++j) {
+                    const double c = S.cs[j - 1], sn = S.sn[j - 1];
+                    const double tmp = __dadd_rn(__dmul_rn(c, hrun), __dmul_rn(sn, h[j]));
+                    hrun = __dadd_rn(__dmul_rn(-sn, hrun), __dmul_rn(c, h[j]));
+                    S.H[(j - 1) * kLsMaxK + kk] = tmp;
+                }
+                const double den = hypot(hrun, nrm);
+                const double c = __ddiv_rn(hrun, den), sn = __ddiv_rn(nrm, den);
+                S.cs[kk] = c;
+                S.sn[kk] = sn;
+                S.H[kk * kLsMaxK + kk] = den;
+                const double gn = __dmul_rn(-sn, g_k);
+                S.g[kk] = __dmul_rn(c, g_k);
+                S.g[kk + 1] = gn;
+                if (hist) hist[kk + 1] = fabs(gn);
+                g_k = gn;
+                S.stop = brk || (tol >= 0.0 && fabs(gn) <= __dmul_rn(tol, beta));
+            }
+            done = kk + 1;
+        }
+        __syncthreads();
+        if (!skip && tid < 32) {
+            double acc = lane < done ? S.g[lane] : 0.0;
+            for (int j = done - 1; j >= 0; --j) {
+                double yj = 0.0;
+                if (lane == j) yj = __ddiv_rn(acc, S.H[j * kLsMaxK + j]);
+                yj = __shfl_sync(0xffffffffu, yj, j);
+                if (lane == j) S.y[j] = yj;
+                if (lane < j) acc = __dsub_rn(acc, __dmul_rn(S.H[lane * kLsMaxK + j], yj));
+            }
+        }
+        __syncthreads();
+        // x = sum_j b_j y_j, output form (bank A: its last readers passed a barrier since)
+        for_nodes_nv(std::integral_constant<int, 1>{}, 0, [&](int64_t i, int, int, double *acc) {
+            double x = 0.0;
+            if (anybad) {
+                x = __longlong_as_double(0x7ff8000000000000LL);
+            } else if (!skip) {
+                for (int j = 0; j < done; ++j) x = fma(basis[(int64_t)j * n + i], S.y[j], x);
+            }
+            const double g = a.G ? a.G[b * a.ld_g + i] : 0.0;
+            x = a.U_sub ? __dsub_rn(__dadd_rn(g, x), a.U_sub[b * a.ld_sub + i]) : __dadd_rn(x, g);
+            if (a.out) a.out[b * a.ld_out + i] = x;
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(x, x));
+        });
+        gtotals(0, 1, tot);
+        if (tid == 0 && chunk == 0) {
+            if (a.partial) a.partial[b] = tot[0];
+            if (C.gmres_iters) C.gmres_iters[b] = anybad ? -1 : done;
+        }
+        ssync();
+    }
+}
+
 int tiles_for(int64_t n) { return (int)((n + kTile2 - 1) / kTile2); }
 
 int coop_capacity(const void *fn) {
@@ -688,6 +972,14 @@ static int64_t coop_rows_cap(const mgrit_level_desc *L);
 // the cooperative GMRES instantiation a level dispatches to: p = 3 on the
 // 512-wide mesh and p = 5 on the 1024-wide mesh use compile-time row strides
 static const void *coop_fn(const mgrit_level_desc *L) {
+    if (L->gmres_lowsync && L->gmres_max_iters <= kLsMaxK) {
+        switch (L->p) {
+            case 1: return (const void *)gmres2d_coop_ls<1>;
+            case 3: return L->n_x == 512 ? (const void *)gmres2d_coop_ls<3, 512> : (const void *)gmres2d_coop_ls<3>;
+            default:
+                return L->n_x == 1024 ? (const void *)gmres2d_coop_ls<5, 1024> : (const void *)gmres2d_coop_ls<5>;
+        }
+    }
     switch (L->p) {
         case 1: return (const void *)gmres2d_coop<1>;
         case 3: return L->n_x == 512 ? (const void *)gmres2d_coop<3, 512> : (const void *)gmres2d_coop<3>;
@@ -729,7 +1021,9 @@ static int64_t coop_rows_cap(const mgrit_level_desc *L) {
 
 static int64_t coop_row_bytes(const mgrit_level_desc *L) {
     const int64_t n = L->n_points, nwb = (n + kWB - 1) / kWB;
-    return 8 * ((int64_t)(L->gmres_max_iters + 3) * n + 2 * nwb) + 4 * 4096 + 8;
+    // basis (K+1) + two Arnoldi vectors, the reduction partials (two banks for
+    // the classic loop, 2K+2 arrays for the low-sync one), flags, barrier word
+    return 8 * ((int64_t)(L->gmres_max_iters + 3) * n + (int64_t)kLsVals * nwb) + 4 * 4096 + 8;
 }
 
 int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows) {
@@ -746,19 +1040,19 @@ int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows) {
 
 template <int P, bool SO>
 static void launch_strip(int nb, dim3 g, const mgrit_level_desc *L, const Rows2D &s, cudaStream_t st) {
+    const int64_t jobs = (int64_t)g.x * g.y;
     auto go = [&](auto NBC) {
         constexpr int NB = decltype(NBC)::value;
+        auto run = [&](auto fn) { fn<<<(unsigned)jobs, kNT2, 0, st>>>(*L, s, jobs); };
         if (P == 5 && L->n_x == 1024)
-            sl2d_strip_kernel<P, NB, SO, (P == 5 ? 1024 : 0)><<<g, kNT2, 0, st>>>(*L, s);
+            run(sl2d_strip_kernel<P, NB, SO, (P == 5 ? 1024 : 0)>);
         else if (P == 3 && L->n_x == 512)
-            sl2d_strip_kernel<P, NB, SO, (P == 3 ? 512 : 0)><<<g, kNT2, 0, st>>>(*L, s);
+            run(sl2d_strip_kernel<P, NB, SO, (P == 3 ? 512 : 0)>);
         else
-            sl2d_strip_kernel<P, NB, SO, 0><<<g, kNT2, 0, st>>>(*L, s);
+            run(sl2d_strip_kernel<P, NB, SO, 0>);
     };
     if (nb == 2)
         go(std::integral_constant<int, 2>{});
-    else if (nb == 8)
-        go(std::integral_constant<int, 8>{});
     else
         go(std::integral_constant<int, 4>{});
 }
@@ -809,7 +1103,7 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             C.w = C.basis + rows * (int64_t)(L->gmres_max_iters + 1) * n;
             C.w2 = C.w + rows * n;
             C.part = C.w2 + rows * n;
-            C.flags = (int *)(C.part + 2 * rows * nwb);
+            C.flags = (int *)(C.part + (int64_t)kLsVals * rows * nwb);
             C.bar = (unsigned int *)(C.flags + rows * chunks);
             if (cudaMemsetAsync(C.bar, 0, rows * sizeof(unsigned int), st) != cudaSuccess) {
                 set_error("cudaMemsetAsync", cudaGetLastError());

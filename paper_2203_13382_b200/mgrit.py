@@ -222,6 +222,9 @@ class Level:
     finer: "Level | None" = None
     shared: bool = False
     stencil_numba: bool = False
+    # first step whose records/sigma are stored (a time-sharded hierarchy keeps
+    # only the steps its rank group works on; 0 = all steps)
+    set0: int = 0
 
     # -- read-only views of the reference's Level data (mgrit.py:89-117) -----
 
@@ -272,15 +275,19 @@ class Level:
         d.shared = int(self.shared)
         d.n_steps = self.n_steps
         d.n_points = self.grid.n_points
-        d.s_x = _ptr(self.s_x)
-        d.s_y = _ptr(self.s_y)
-        d.sig_x = _ptr(self.sig_x)
-        d.sig_y = _ptr(self.sig_y)
+        # kernels address step t's record at base + t * n_points: a sharded
+        # level passes its base shifted by the first stored step (only the
+        # stored steps are ever addressed)
+        off = 0 if self.shared else self.set0 * self.grid.n_points * 8
+        d.s_x = _ptr(self.s_x) - off if self.s_x is not None else 0
+        d.s_y = _ptr(self.s_y) - off if self.s_y is not None else 0
+        d.sig_x = _ptr(self.sig_x) - off if self.sig_x is not None else 0
+        d.sig_y = _ptr(self.sig_y) - off if self.sig_y is not None else 0
         g = self.gmres_cfg or GmresConfig()
         d.gmres_max_iters = g.max_iters
         d.gmres_tol = -1.0 if g.tol is None else float(g.tol)
         d.stencil_numba = int(self.stencil_numba if stencil_numba is None else stencil_numba)
-        d.gmres_lowsync = int(g.variant == "mgs_lowsync" and self.grid.dim == 1)
+        d.gmres_lowsync = int(g.variant == "mgs_lowsync")
         d.launch_policy = LAUNCH_POLICIES[_launch_policy]
         return d
 
@@ -383,13 +390,13 @@ def _alloc_records(S, n, dim, dev):
     return s_x, s_y, d_x, d_y
 
 
-def _erk(grid, speed: WaveSpeed, order, S, dt, n_sub, dt_sub, dev):
+def _erk(grid, speed: WaveSpeed, order, S, dt, n_sub, dt_sub, dev, set_first: int = 0):
     if speed.device is None:
         raise ValueError(f"wave speed {speed.name!r} has no device form; pass fine_coords= to build_hierarchy")
     s_x, s_y, d_x, d_y = _alloc_records(S, grid.n_points, grid.dim, dev)
     tab = _lib.erk_tableau(order)
     rc = _lib.load().mgrit_erk_departures(grid.dim, grid.n_x, _lib.SPEED_IDS[speed.device], ctypes.byref(tab),
-                                          0, S, float(dt), int(n_sub), float(dt_sub), s_x.data_ptr(),
+                                          int(set_first), S, float(dt), int(n_sub), float(dt_sub), s_x.data_ptr(),
                                           _ptr(s_y), d_x.data_ptr(), _ptr(d_y), stream_ptr())
     _lib.check(rc, "erk_departures")
     return s_x, s_y, d_x, d_y

@@ -378,9 +378,8 @@ def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: boo
     # initial residual over the owned steps (row0+1 .. row0+local_rows-1)
     nloc = p0.local_rows - 1
     row_ss = torch.empty(nloc, dtype=torch.float64, device=dev)
-    R = torch.empty((nloc, n), dtype=torch.float64, device=dev)
-    levels[0]._apply(U, p0.row0, 1, nloc, R, U_sub=U[1:], row_sumsq=row_ss)
-    del R
+    # only the per-row sums of squares are produced (out = NULL: no residual rows)
+    levels[0]._apply(U, p0.row0, 1, nloc, None, U_sub=U[1:], row_sumsq=row_ss)
     row_all = torch.empty(cfg.n_t, dtype=torch.float64, device=dev)
     comm.allgather_groups(row_all, row_ss, p0.stride)
     s0 = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -414,3 +413,102 @@ def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: boo
     fac = float(h[-1] / h[-2]) if len(h) > 1 else float("nan")
     wall = time.perf_counter() - t0
     return ConvergenceReport(h, len(h) - 1, state, fac, wall, 0.0, wall), U, p0
+
+
+# ---------------------------------------------------------------------------
+# sharded hierarchy construction
+
+
+def build_hierarchy_sharded(cfg, comm: Comm | None = None):
+    """``build_hierarchy`` (mgrit.py:217-269) for a time-sharded solve.
+
+    Every rank traces (ERK), backtracks and computes sigma only for the steps
+    its rank group works on: on level l the steps of the group's intervals,
+    all steps on the replicated coarsest level.  Coarse step c of level l is
+    interval c of level l-1, so the rank that owns that interval holds its m
+    children and builds the step locally; where level l is split over fewer
+    groups than level l-1 (or replicated) the built slabs are all-gathered
+    (``Comm.allgather_groups``) and the group's range is kept.  Records are
+    bit-identical to the replicated build's (same kernels on the same data)
+    and per-rank record memory drops from all n_t fine steps to n_t / P.
+    A level stores steps [set0, set0 + S_local); the kernels address the
+    stored rows through the level descriptor (``Level.desc``)."""
+    from . import mgrit as M
+    from .core import Grid1D, Grid2D, require_cuda, stream_ptr
+
+    comm = comm or Comm()
+    speed = cfg.speed
+    if comm.size == 1 or speed.constant or cfg.operator_kind == "ideal":
+        return M.build_hierarchy(cfg)     # one shared record set / composed operator: nothing to shard
+    if cfg.departure_policy != "backtrack":
+        return M.build_hierarchy(cfg)
+    dev = require_cuda()
+    grid = Grid1D(cfg.n_x) if cfg.dim == 1 else Grid2D(cfg.n_x)
+    n = grid.n_points
+    dt = cfg.dt if cfg.dt is not None else M.DEFAULT_CFL * grid.h
+    lib = _lib.load()
+    # level sizes / factors exactly as build_hierarchy derives them
+    sizes, factors = [cfg.n_t], []
+    while cfg.max_levels is None or len(sizes) < cfg.max_levels:
+        m = cfg.schedule_factor(len(sizes) - 1)
+        if sizes[-1] % m != 0 or sizes[-1] // m < 2:
+            break
+        factors.append(m)
+        sizes.append(sizes[-1] // m)
+    if len(sizes) < 2:
+        raise ValueError("time grid does not admit any coarsening with the given schedule")
+    factors.append(None)
+    plans = make_plan(sizes, factors, comm.rank, comm.size)
+
+    def need(li):
+        p = plans[li]
+        return (0, p.n_steps) if p.m is None else (p.cb * p.m, p.ce * p.m)
+
+    def rows(t, first):          # pointer to stored row `first` of a (S, n) tensor (0 if absent)
+        return 0 if t is None else t.data_ptr() + first * n * 8
+
+    a, b = need(0)
+    s_x, s_y, d_x, d_y = M._erk(grid, speed, cfg.erk_order, b - a, dt, 1, dt, dev, set_first=a)
+    fine = M.Level(0, grid, cfg.p, cfg.n_t, dt, "fine", s_x, s_y, d_x, d_y, set0=a)
+    levels = [fine]
+    for li in range(1, len(sizes)):
+        prev, pp, m = levels[-1], plans[li - 1], factors[li - 1]
+        c0, c1 = pp.cb, pp.ce                       # coarse steps whose children this rank holds
+        cnt = c1 - c0
+        off = c0 * m - prev.set0                    # first child's stored row
+        s_x, s_y, d_x, d_y = M._alloc_records(cnt, n, grid.dim, dev)
+        _lib.check(lib.mgrit_backtrack(grid.dim, grid.n_x, m, cnt, 0, rows(prev.disp_x, off),
+                                       rows(prev.disp_y, off), s_x.data_ptr(), M._ptr(s_y), d_x.data_ptr(),
+                                       M._ptr(d_y), stream_ptr()), "backtrack")
+        sig_x = sig_y = None
+        if cfg.operator_kind in ("corrected", "forward_euler"):
+            sig_x = torch.empty((cnt, n), dtype=torch.float64, device=dev)
+            sig_y = torch.empty_like(sig_x) if grid.dim == 2 else None
+            _lib.check(lib.mgrit_phi_sigma(grid.dim, grid.n_x, cfg.p, m, cnt, 0, s_x.data_ptr(), M._ptr(s_y),
+                                           rows(prev.s_x, off), rows(prev.s_y, off), rows(prev.sig_x, off),
+                                           rows(prev.sig_y, off), sig_x.data_ptr(), M._ptr(sig_y), stream_ptr()),
+                       "phi_sigma")
+        a, b = need(li)
+        if (a, b) != (c0, c1):
+            # the level is split over fewer groups than its parent: gather every
+            # group's slab (one per parent group, in order), keep this group's range
+            def gather(t):
+                if t is None:
+                    return None
+                full = torch.empty((sizes[li], n), dtype=torch.float64, device=dev)
+                comm.allgather_groups(full, t, pp.stride)
+                return full[a:b].clone()
+            s_x, s_y, d_x, d_y, sig_x, sig_y = (gather(t) for t in (s_x, s_y, d_x, d_y, sig_x, sig_y))
+        lvl = M.Level(li, grid, cfg.p, sizes[li], prev.dt * m, cfg.operator_kind, s_x, s_y, d_x, d_y, sig_x, sig_y,
+                      finer=prev, set0=a)
+        prev.cf = m
+        prev.disp_x = prev.disp_y = None
+        levels.append(lvl)
+    levels[-1].disp_x = levels[-1].disp_y = None
+    mode = cfg.gmres_mode or ("fixed" if len(levels) == 2 else "tolerance")
+    gcfg = M.GmresConfig(10, None if mode == "fixed" else 1e-2, cfg.gmres_variant)
+    for lvl in levels[1:]:
+        lvl.gmres_cfg = gcfg
+    last = levels[-1]
+    last.stencil_numba = (last.grid.dim == 1 and last.kind == "corrected" and last.n_steps >= 64)
+    return levels

@@ -178,7 +178,27 @@ def run_oracle(name, kw, max_iters):
     rec.save(status)
 
 
+def compact(name, norm_stride, col_stride):
+    """Keep every norm_stride-th row norm and every col_stride-th row of the
+    sampled columns (plus the last row), so large fixtures stay a few MB."""
+    path = os.path.join(HERE, f"solve_{name}.npz")
+    g = dict(np.load(path))
+    n_rows = g["row_norms"].shape[1]
+    nr = np.unique(np.append(np.arange(0, n_rows, norm_stride), n_rows - 1))
+    cr = np.unique(np.append(np.arange(0, n_rows, col_stride), n_rows - 1))
+    if "norm_rows" in g:
+        raise SystemExit(f"{name} is already compact")
+    g["row_norms"] = g["row_norms"][:, nr]
+    g["cols"] = g["cols"][:, cr]
+    g["norm_rows"], g["cols_rows"] = nr, cr
+    np.savez_compressed(path, **g)
+    print(f"[fullsize] {name}: kept {len(nr)} row norms and {len(cr)} column rows of {n_rows}")
+
+
 def main(argv):
+    if argv[0] == "compact":
+        compact(argv[1], int(argv[2]), int(argv[3]))
+        return
     name = argv[0] if argv[0] in CASES else f"{argv[0]}_full"
     kw = CASES[name]
     if name in REFERENCE_CASES:

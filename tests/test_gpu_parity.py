@@ -291,12 +291,14 @@ def test_solve_matches_reference_golden(P, golden_index, name):
     _check_solve(rep, U, info, g, exact_records=False, name=name)
 
 
+@pytest.mark.parametrize("variant", ["mgs", "mgs_lowsync"])
 @pytest.mark.parametrize("name", SOLVES_2D)
-def test_solve_2d_matches_reference_golden(P, golden_index, name):
-    """2D: device ERK + device hierarchy + fused 2D phases vs the reference's history."""
+def test_solve_2d_matches_reference_golden(P, golden_index, name, variant):
+    """2D: device ERK + device hierarchy + fused 2D phases vs the reference's
+    history, with the classic and the low-sync cooperative GMRES."""
     info = golden_index[name]
     g = load_solve(name)
-    rep, U = P.solve(P.SolverConfig(**info["kw"]))
+    rep, U = P.solve(P.SolverConfig(**info["kw"], gmres_variant=variant))
     _check_solve(rep, U, info, g, exact_records=False, name=name)
 
 

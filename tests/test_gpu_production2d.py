@@ -89,7 +89,26 @@ def test_sl2d_cfg5_mesh_p5_bitwise(P, cfg5_mesh):
         assert np.array_equal(got[b], ol.step(t, U[b])), t
 
 
-def _corrected_rows(lv, steps, seed):
+VARIANTS = ["mgs", "mgs_lowsync"]
+
+
+def _with_variant(lv, variant):
+    """The level with its GMRES loop switched to `variant` (restored by the caller)."""
+    import dataclasses
+    prev = lv.gmres_cfg
+    lv.gmres_cfg = dataclasses.replace(prev, variant=variant)
+    return prev
+
+
+def _corrected_rows(lv, steps, seed, variant="mgs"):
+    prev = _with_variant(lv, variant)
+    try:
+        return _corrected_rows_impl(lv, steps, seed)
+    finally:
+        lv.gmres_cfg = prev
+
+
+def _corrected_rows_impl(lv, steps, seed):
     ol = _oracle_level(lv, steps)
     log = O.GmresLog()
     ol.log = log
@@ -106,12 +125,14 @@ def _corrected_rows(lv, steps, seed):
     return log.counts
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("li,steps", [(1, [0, 5, 9, 15]), (2, [0, 1])])
-def test_corrected_cfg5_mesh_gmres2d_coop_5_1024(P, cfg5_mesh, li, steps):
-    """Config 5's corrected levels: gmres2d_coop<5, 1024> with 2 systems in
-    flight per round (L2-sized) over ~296 CTAs each; 4 rows = 2 rounds."""
+def test_corrected_cfg5_mesh_gmres2d_coop_5_1024(P, cfg5_mesh, li, steps, variant):
+    """Config 5's corrected levels: gmres2d_coop<5, 1024> (and its low-sync
+    form) with 2 systems in flight per round (L2-sized) over ~296 CTAs each;
+    4 rows = 2 rounds."""
     _, levels = cfg5_mesh
-    counts = _corrected_rows(levels[li], steps, seed=li)
+    counts = _corrected_rows(levels[li], steps, seed=li, variant=variant)
     assert all(c >= 1 for c in counts)
 
 
@@ -121,27 +142,31 @@ def cfg4_mesh(P):
     return cfg, P.build_hierarchy(cfg)
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("li,steps", [(1, [0, 3, 7, 8, 12, 15]), (2, [0, 1, 2, 3])])
-def test_corrected_cfg4_mesh_gmres2d_coop_3_512(P, cfg4_mesh, li, steps):
+def test_corrected_cfg4_mesh_gmres2d_coop_3_512(P, cfg4_mesh, li, steps, variant):
     """Config 4's corrected levels through gmres2d_coop<3, 512>."""
     _, levels = cfg4_mesh
-    _corrected_rows(levels[li], steps, seed=10 + li)
+    _corrected_rows(levels[li], steps, seed=10 + li, variant=variant)
 
 
-@pytest.mark.parametrize("p", [3, 5])
-def test_corrected_256_mesh_row_blocks_multichunk(P, p):
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("p", [1, 3, 5])
+def test_corrected_256_mesh_row_blocks_multichunk(P, p, variant):
     """The generic instantiation on a 256^2 mesh: row-block addressing
     (n_x % 256 == 0), every system split over many CTAs that all hold data,
     and more systems than slots."""
     cfg = P.SolverConfig(n_x=256, n_t=64, dim=2, wave_speed="B4", p=p, schedule=4, seed=3)
     levels = P.build_hierarchy(cfg)
-    _corrected_rows(levels[1], list(range(16)), seed=p)
+    _corrected_rows(levels[1], list(range(16)), seed=p, variant=variant)
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("mode", ["fixed", "tolerance"])
-def test_corrected_cfg5_mesh_fixed_and_tol(P, mode):
+def test_corrected_cfg5_mesh_fixed_and_tol(P, mode, variant):
     """Both GMRES modes at 1024^2 (fixed K = 10 runs every Arnoldi step)."""
-    cfg = P.SolverConfig(n_x=1024, n_t=16, dim=2, wave_speed="B4", p=5, schedule=8, seed=4, gmres_mode=mode)
+    cfg = P.SolverConfig(n_x=1024, n_t=16, dim=2, wave_speed="B4", p=5, schedule=8, seed=4, gmres_mode=mode,
+                         gmres_variant=variant)
     levels = P.build_hierarchy(cfg)
     lv = levels[1]
     steps = [0, 1]
@@ -229,6 +254,8 @@ def _check_fullsize(P, g, levels, it_tol):
             Uj = U
         norms = _np(torch.linalg.vector_norm(Uj, dim=1))
         cols = _np(Uj[:, idx])
+        if "norm_rows" in g:          # compacted fixture: a subset of the rows
+            norms, cols = norms[g["norm_rows"]], cols[g["cols_rows"]]
         rel_n = float(np.max(np.abs(norms - g["row_norms"][j - 1]) / np.maximum(g["row_norms"][j - 1], 1e-300)))
         rel_c = _rel(cols, g["cols"][j - 1])
         worst = max(worst, rel_n, rel_c)

@@ -34,7 +34,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, size, port, kw, out):
+def _worker(rank, size, port, kw, out, build="replicated"):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -44,8 +44,14 @@ def _worker(rank, size, port, kw, out):
         import paper_2203_13382_b200 as P
         from paper_2203_13382_b200 import timepar as T
         cfg = P.SolverConfig(**kw)
-        levels = P.build_hierarchy(cfg)
-        rep, U, p0 = T.solve_time_parallel(cfg, levels, T.Comm())
+        comm = T.Comm()
+        if build == "sharded":
+            levels = T.build_hierarchy_sharded(cfg, comm)
+            # records of the owned steps only (1/P of the fine level)
+            assert levels[0].s_x.shape[0] == cfg.n_t // size
+        else:
+            levels = P.build_hierarchy(cfg)
+        rep, U, p0 = T.solve_time_parallel(cfg, levels, comm)
         rows = U[1:].cpu()
         allr = [torch.empty_like(rows) for _ in range(size)]
         dist.all_gather(allr, rows)
@@ -58,13 +64,17 @@ def _worker(rank, size, port, kw, out):
 
 @pytest.mark.parametrize("name", list(CASES))
 @pytest.mark.parametrize("ranks", [2, 4])
-def test_sharded_cuda_engine_equals_single_rank(tmp_path, name, ranks):
+@pytest.mark.parametrize("build", ["replicated", "sharded"])
+def test_sharded_cuda_engine_equals_single_rank(tmp_path, name, ranks, build):
+    """Replicated hierarchy, or the per-rank sharded build (each rank traces /
+    backtracks / computes sigma only for its group's steps): both reproduce
+    the single-GPU solve bit for bit."""
     import paper_2203_13382_b200 as P
     kw = CASES[name]
     if (kw["n_t"] // kw["schedule"]) % ranks:
         pytest.skip("fine level not divisible")
     out = str(tmp_path / "r.npz")
-    mp.spawn(_worker, args=(ranks, _free_port(), kw, out), nprocs=ranks, join=True)
+    mp.spawn(_worker, args=(ranks, _free_port(), kw, out, build), nprocs=ranks, join=True)
     got = np.load(out)
     cfg = P.SolverConfig(**kw)
     rep, U = P.solve(cfg)
