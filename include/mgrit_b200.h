@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define MGRIT_ABI_VERSION 2
+#define MGRIT_ABI_VERSION 3
 
 enum { MGRIT_OK = 0, MGRIT_EINVAL = 2, MGRIT_ECUDA = 3 };
 /* launch policy of corrected 1D phases / sweeps: AUTO picks the cluster-split
@@ -80,6 +80,15 @@ typedef struct mgrit_level_desc {
                                block reductions are cheaper there) */
     int32_t launch_policy;  /* MGRIT_LAUNCH_*: corrected 1D levels may run one
                                thread-block cluster (2-16 SMs) per row chain */
+    int32_t sl2d_separable; /* 2D: set ONLY from mgrit_records_separable() on these
+                               very record arrays.  1 = s_x does not depend on the
+                               mesh row and s_y not on the column (bitwise), so a
+                               plain SL step reads one x-record per column (mesh
+                               row 0) and one y-record per row (column 0) instead
+                               of 16 B per node, and shares each source row's
+                               x-interpolation down a column (bit-identical rows).
+                               0 = every node's own records are read. */
+    int32_t pad_;
 } mgrit_level_desc;
 
 /* ERK tableau for departure tracing (semi_lagrangian.py:46-72); built on the
@@ -128,6 +137,15 @@ int mgrit_backtrack(int32_t dim, int32_t n_x, int32_t m, int64_t n_sets,
                     int32_t child_shared, const double *child_disp_x,
                     const double *child_disp_y, double *s_x, double *s_y,
                     double *disp_x, double *disp_y, void *stream);
+
+/* 2D: *flag (device int32) = 1 iff in every one of the n_sets record sets s_x is
+ * bitwise independent of the mesh row and s_y of the mesh column -- true when
+ * the x-speed depends on (x, t) only and the y-speed on (y, t) only, as for
+ * BASELINE's 2D speed: erk_trace_back (semi_lagrangian.py:75-115) then traces
+ * every row / column with identical operands.  Every record is compared.  The
+ * only valid source of mgrit_level_desc::sl2d_separable. */
+int mgrit_records_separable(int32_t n_x, int64_t n_sets, const double *s_x,
+                            const double *s_y, int32_t *flag, void *stream);
 
 /* sigma = phi(eps_coarse, eps_children) [+ sum_k sigma_child_k]
  * (phi_field / sigma_accumulate, coarse_correction.py:92-127; mgrit.py:249-256).

@@ -29,6 +29,7 @@ class LevelDesc(ctypes.Structure):
         ("s_x", c_vp), ("s_y", c_vp), ("sig_x", c_vp), ("sig_y", c_vp),
         ("gmres_max_iters", c_i32), ("stencil_numba", c_i32), ("gmres_tol", c_dbl),
         ("gmres_lowsync", c_i32), ("launch_policy", c_i32),
+        ("sl2d_separable", c_i32), ("pad_", c_i32),
     ]
 
 
@@ -60,6 +61,7 @@ _SIGS = {
     "mgrit_backtrack": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mgrit_phi_sigma": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        c_vp, c_vp, c_vp, c_vp]),
+    "mgrit_records_separable": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "mgrit_pcg64_fill": (ctypes.c_int, [c_u64, c_u64, c_u64, c_u64, c_i64, c_i32, c_vp, c_vp]),
     "mgrit_apply_rows": (ctypes.c_int, [ctypes.POINTER(LevelDesc), c_i64, c_vp, c_i64, c_i64, c_vp, c_i64,
                                         c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
@@ -107,7 +109,7 @@ def load(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.mgrit_abi_version() != 2:
+    if lib.mgrit_abi_version() != 3:
         raise RuntimeError("libmgrit_b200.so ABI mismatch")
     if path is None:
         _LIB = lib

@@ -117,6 +117,11 @@ extern "C" int mgrit_sequential_sweep(const mgrit_level_desc *L, double *U, int6
     return MGRIT_EINVAL;
 }
 
+extern "C" int mgrit_records_separable(int32_t n_x, int64_t n_sets, const double *s_x, const double *s_y,
+                                       int32_t *flag, void *stream) {
+    return records_separable_2d(n_x, n_sets, s_x, s_y, flag, (cudaStream_t)stream);
+}
+
 extern "C" int mgrit_sum(const double *x, int64_t n, double *out, void *stream) {
     if (n < 0 || !out || (n > 0 && !x)) return MGRIT_EINVAL;
     sum_kernel<<<1, kSumThreads, 0, (cudaStream_t)stream>>>(x, n, out);

@@ -37,6 +37,8 @@ int level_phase_2d(const mgrit_level_desc *L, const mgrit_phase_args *A, void *s
                    int32_t *status, cudaStream_t st);
 int sweep_2d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G, int64_t ldg, int zero_init,
              int32_t *gmres_iters, void *scratch, int64_t scratch_bytes, int32_t *status, cudaStream_t st);
+int records_separable_2d(int32_t n_x, int64_t n_sets, const double *s_x, const double *s_y, int32_t *flag,
+                         cudaStream_t st);
 int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows);
 int64_t capacity2d(const mgrit_level_desc *L);
 int axpy_rows_impl(double *U, int64_t ldu, int64_t stride, const double *X, int64_t ldx, int64_t rows,

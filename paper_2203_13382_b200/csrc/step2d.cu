@@ -341,6 +341,224 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_strip_kernel(mgrit_level_desc L,
     }
 }
 
+// Separable SL step.  When a level's x-records do not depend on the mesh row
+// and its y-records do not depend on the column (bitwise; BASELINE's 2D speed
+// (cos^2(pi x) cos(2 pi t) + 0.5, sin^2(pi y) cos(2 pi t) + 0.5) traces such
+// departures, and mgrit_records_separable() verifies it over every record of
+// the level at setup), the tensor-product gather factorises: the
+// x-interpolation T[r][ix] = sum_jx wx[ix][jx] u[r][ex(ix) - l + jx] of a
+// source row r is the same rounded value for every node of column ix that
+// uses row r, and the y-weights of a mesh row are the same in every column.
+//
+// A CTA owns 256 columns x nb mesh rows, one column per thread.
+//   1. The x-record of each column is read from mesh row 0 of the set and the
+//      y-record of each row from column 0 (8 B per column / row instead of
+//      16 B per node: the step's HBM traffic drops from 32 to 16 B per node).
+//   2. The source tile the band touches (nb + p rows plus the drift of the
+//      y-departures, 256 + p columns plus the drift of the x-departures) is
+//      staged in shared memory with 16-byte cp.async copies, all in flight at
+//      once: one DRAM round trip per CTA, four CTAs per SM.
+//   3. Each thread slides a register window of p + 1 row sums down its column
+//      (every source row is x-interpolated once per column, taps from shared
+//      memory); thread k < nb derived mesh row k's y-weights once for the CTA,
+//      and every node is the reference's own y-combination of the window.
+// Each node's arithmetic is exactly semi_lagrangian.py:238-253 (x inner from
+// 0, y outer from 0, separately rounded products), so rows are bit-identical
+// to the per-node kernels; only identical subexpressions are shared.  Per
+// node-update at p = 5, nb = 16: ~27 FP64 instructions (per-node kernel: 185),
+// which takes the step off the FP64-issue bound.
+//
+// A tile whose source rows or columns do not fit the staged tile (large-CFL
+// coarse levels) gathers per node from the same two reference records.
+//
+// Row norms: partial sums are formed per 256 x kSepSub sub-block, whatever nb
+// is, so a row's sum of squares does not depend on the batch size.
+constexpr int kSepMaxRows = 32;
+constexpr int kSepSub = 8;
+constexpr int kSepSlack = 2;   // staged rows beyond nb + p
+constexpr int kSepW = 264;     // staged columns (256 + p + drift + alignment), even
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+                 : "memory");
+}
+
+template <int P, bool SLONLY>
+__global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, Rows2D a, int nb, int cap, int64_t jobs) {
+    extern __shared__ __align__(16) double s_raw[];   // [cap][kSepW] staged source tile
+    __shared__ __align__(16) double s_wy[kSepMaxRows][P + 1];
+    __shared__ double s_sy[kSepMaxRows];
+    __shared__ int s_ey[kSepMaxRows];
+    __shared__ int s_cmin[kNT2 / 32], s_cmax[kNT2 / 32];
+    __shared__ double red[kNT2 / 32 + 1];
+    constexpr int SL = Stencil<P>::L;
+    const int nx = L.n_x;
+    const int64_t n = (int64_t)nx * nx;
+    const int tiles_x = nx / kNT2;
+    const int64_t tiles = (int64_t)tiles_x * (nx / nb);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t j = blockIdx.x;
+    if (j >= jobs) return;
+    const int64_t b = j / tiles, tile = j - b * tiles;
+    const int band = (int)(tile / tiles_x);
+    const int ix = (int)(tile - (int64_t)band * tiles_x) * kNT2 + tid;
+    const int iy0 = band * nb;
+    const int64_t set = L.shared ? 0 : row_t(a, b);
+    const int64_t i0 = (int64_t)iy0 * nx + ix;
+    const double *u = a.U_in + b * a.ld_in;
+
+    // column ix's x-record (mesh row 0) and mesh row k's y-record (column 0)
+    const double sx0 = __ldg(L.s_x + set * n + ix);
+    if (tid < nb) {
+        const double s = __ldg(L.s_y + set * n + (int64_t)(iy0 + tid) * nx);
+        const Dec d = decompose_s(s, nx);
+        double w[P + 1];
+        lagrange_weights<P>(d.eps, w);
+        s_sy[tid] = s;
+        s_ey[tid] = (unsigned)d.e < (unsigned)nx ? d.e : -1;
+#pragma unroll
+        for (int q = 0; q <= P; ++q) s_wy[tid][q] = w[q];
+    }
+    const Dec dx = decompose_s(sx0, nx);
+    const bool xok = (unsigned)dx.e < (unsigned)nx;
+    // first tap column, as the periodic image nearest to the node's own column
+    int c0 = (xok ? dx.e : ix) - SL;
+    if (2 * (c0 - ix) > nx) c0 -= nx;
+    if (2 * (c0 - ix) < -nx) c0 += nx;
+    {
+        const int mn = __reduce_min_sync(0xffffffffu, c0), mx = __reduce_max_sync(0xffffffffu, c0);
+        if (lane == 0) {
+            s_cmin[warp] = mn;
+            s_cmax[warp] = mx;
+        }
+    }
+    const bool allx = __syncthreads_and(xok);
+    int cmin = s_cmin[0], cmax = s_cmax[0];
+#pragma unroll
+    for (int w = 1; w < kNT2 / 32; ++w) {
+        cmin = min(cmin, s_cmin[w]);
+        cmax = max(cmax, s_cmax[w]);
+    }
+    const int colbase = cmin & ~1;                 // even: 16-byte aligned copies
+    const int width = cmax + P + 1 - colbase;      // staged columns
+    // source-row window of the band: east rows relative to the first one
+    // (periodic, nearest image), first row and span
+    const int e_first = s_ey[0];
+    auto rel_of = [&](int e) {
+        int r = e - e_first;
+        if (2 * r < -nx) r += nx;
+        if (2 * r > nx) r -= nx;
+        return r;
+    };
+    int lo = 0, hi = 0;
+    bool rows_ok = true;
+    for (int k = 0; k < nb; ++k) {
+        const int e = s_ey[k];
+        rows_ok = rows_ok && e >= 0;
+        const int r = rel_of(e);
+        lo = r < lo ? r : lo;
+        hi = r > hi ? r : hi;
+    }
+    const int span = hi - lo + P + 1;
+    const bool staged = allx && rows_ok && span <= cap && width <= kSepW;
+
+    const double *gp = (!SLONLY && a.G) ? a.G + b * a.ld_g + i0 : nullptr;
+    const double *up = (!SLONLY && a.U_sub) ? a.U_sub + b * a.ld_sub + i0 : nullptr;
+    double *op = a.out ? a.out + b * a.ld_out + i0 : nullptr;
+    double *pp = (!SLONLY && a.partial) ? a.partial + b * (n / ((int64_t)kNT2 * kSepSub)) +
+                                              (int64_t)(iy0 / kSepSub) * tiles_x + (ix / kNT2)
+                                        : nullptr;
+    double ss = 0.0;
+    // output form of node (ix, iy0 + k) (as sl2d_kernel) and the sub-block partials
+    auto emit = [&](int k, double x) {
+        const int64_t ko = (int64_t)k * nx;
+        if constexpr (!SLONLY) {
+            const double g = gp ? gp[ko] : 0.0;
+            x = up ? __dsub_rn(__dadd_rn(g, x), up[ko]) : __dadd_rn(x, g);
+            ss = __dadd_rn(ss, __dmul_rn(x, x));
+        }
+        if (op) op[ko] = x;
+        if constexpr (!SLONLY) {
+            if (pp && (k & (kSepSub - 1)) == kSepSub - 1) {
+                const double tot = block_sum<kNT2>(ss, red);
+                if (tid == 0) pp[(int64_t)(k / kSepSub) * tiles_x] = tot;
+                ss = 0.0;
+            }
+        }
+    };
+    if (!staged) {   // the band's source window does not fit: per-node gathers
+#pragma unroll 1
+        for (int k = 0; k < nb; ++k) emit(k, sl2d_at<P, 0>(u, nx, sx0, s_sy[k]));
+        return;
+    }
+
+    // stage rows [first, first + span) x columns [colbase, colbase + width) (periodic)
+    {
+        int first = e_first + lo - SL;
+        first = first < 0 ? first + nx : (first >= nx ? first - nx : first);
+        const int wch = (width + 1) >> 1;   // 16-byte chunks per row
+        for (int r = warp; r < span; r += kNT2 / 32) {
+            const int row = first + r >= nx ? first + r - nx : first + r;
+            const double *src = u + (int64_t)row * nx;
+            double *dst = s_raw + r * kSepW;
+            for (int c = lane; c < wch; c += 32) {
+                int col = colbase + 2 * c;
+                col = col < 0 ? col + nx : (col >= nx ? col - nx : col);
+                cp_async16(dst + 2 * c, src + col);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    double wx[P + 1];
+    lagrange_weights<P>(dx.eps, wx);
+    const double *tcol = s_raw + (c0 - colbase);   // this column's first tap in staged row 0
+    auto dot = [&](int r) {
+        const double *t = tcol + r * kSepW;
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q <= P; ++q) acc = __dadd_rn(acc, __dmul_rn(wx[q], t[q]));
+        return acc;
+    };
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+
+    double W[P + 1];   // row sums of the current node's source rows e - l .. e + r
+    int prev = 0;
+    for (int k = 0; k < nb; ++k) {
+        const int rk = rel_of(s_ey[k]) - lo;   // staged row of the node's first source row
+        int d = rk - prev;
+        if (k == 0 || d < 0 || d > P) d = P + 1;
+        for (int q = d - 1; q >= 0; --q) {     // slide the window down by d rows (uniform over the CTA)
+#pragma unroll
+            for (int r = 0; r < P; ++r) W[r] = W[r + 1];
+            W[P] = dot(rk + P - q);
+        }
+        prev = rk;
+        double o = 0.0;
+#pragma unroll
+        for (int q = 0; q <= P; ++q) o = __dadd_rn(o, __dmul_rn(s_wy[k][q], W[q]));
+        emit(k, o);
+    }
+}
+
+// rows per CTA of sl2d_sep_kernel: 16 (a 48 KB table, four CTAs per SM), or 8
+// when that leaves SMs without work (MGRIT_SL2D_SEP_ROWS = 8/16/32 overrides, 0 disables
+// the kernel)
+static int sep_rows(int nx, int64_t B) {
+    // read on every call (a getenv is noise next to a launch) so tests can
+    // switch the strip height within one process
+    const char *e = getenv("MGRIT_SL2D_SEP_ROWS");
+    const int env = e ? atoi(e) : -1;
+    if (env == 0 || nx % kNT2 != 0) return 0;
+    if (env > 0) return (env == 8 || env == 16 || env == 32) && nx % env == 0 ? env : 0;
+    for (int nb = 16; nb >= 8; nb >>= 1) {
+        if (nx % nb != 0) continue;
+        const int64_t jobs = B * (nx / kNT2) * (nx / nb);
+        if (jobs >= 2 * 592 || nb == 8) return nb;
+    }
+    return 0;
+}
+
 // strip height of sl2d_strip_kernel (MGRIT_SL2D_STRIP overrides; 0 = the
 // per-node kernel).  Measured on B200 (tools/gpu_strip_sweep.sh), cfg5 F-step:
 // per-node 4.69 ms, NB = 2 4.11, NB = 4 3.27, NB = 8 3.24 ms (spills; and its
@@ -1057,6 +1275,47 @@ static void launch_strip(int nb, dim3 g, const mgrit_level_desc *L, const Rows2D
         go(std::integral_constant<int, 4>{});
 }
 
+template <int P, bool SO>
+static void launch_sep(int nb, int64_t B, const mgrit_level_desc *L, const Rows2D &s, cudaStream_t st) {
+    const int64_t jobs = B * (L->n_x / kNT2) * (L->n_x / nb);
+    const int cap = nb + P + kSepSlack;
+    const int smem = cap * kSepW * (int)sizeof(double);
+    static int optin = 0;   // per instantiation: largest dynamic size opted in so far
+    if (smem > optin) {
+        cudaFuncSetAttribute(sl2d_sep_kernel<P, SO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        optin = smem;
+    }
+    sl2d_sep_kernel<P, SO><<<(unsigned)jobs, kNT2, smem, st>>>(*L, s, nb, cap, jobs);
+}
+
+// ---------------------------------------------------------------------------
+// separability hint: *flag stays 1 iff, in every record set, s_x does not
+// depend on the mesh row and s_y does not depend on the mesh column (bitwise)
+__global__ void separable_kernel(int nx, int64_t n_sets, const double *s_x, const double *s_y, int32_t *flag) {
+    const int64_t n = (int64_t)nx * nx, total = n_sets * n;
+    bool ok = true;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t set = g / n, i = g - set * n;
+        const int iy = (int)(i / nx), ix = (int)(i - (int64_t)iy * nx);
+        const double *bx = s_x + set * n, *by = s_y + set * n;
+        ok = ok && __double_as_longlong(bx[i]) == __double_as_longlong(bx[ix]) &&
+             __double_as_longlong(by[i]) == __double_as_longlong(by[(int64_t)iy * nx]);
+    }
+    if (!ok) *flag = 0;
+}
+
+__global__ void flag_one_kernel(int32_t *flag) { *flag = 1; }
+
+int records_separable_2d(int32_t n_x, int64_t n_sets, const double *s_x, const double *s_y, int32_t *flag,
+                         cudaStream_t st) {
+    if (n_x < 8 || n_sets < 1 || !s_x || !s_y || !flag) return MGRIT_EINVAL;
+    flag_one_kernel<<<1, 1, 0, st>>>(flag);
+    const int64_t total = n_sets * (int64_t)n_x * n_x;
+    const int64_t blocks = (total + kNT2 - 1) / kNT2;
+    separable_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), kNT2, 0, st>>>(n_x, n_sets, s_x, s_y, flag);
+    return check_launch("separable_kernel");
+}
+
 static int validate2d(const mgrit_level_desc *L) {
     if (!L || L->dim != 2 || L->n_x < 8 || !L->s_x || !L->s_y) return MGRIT_EINVAL;
     if (L->p != 1 && L->p != 3 && L->p != 5) return MGRIT_EINVAL;
@@ -1132,7 +1391,11 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
     // CTA (every BASELINE 2D mesh); the per-node kernel elsewhere
     const int nb = strip_rows();
     const bool strip = nb > 0 && L->n_x % kNT2 == 0 && L->n_x % nb == 0;
-    const int64_t ptiles = strip ? n / ((int64_t)kNT2 * nb) : tiles;
+    // separable records (hinted by the level): the sliding-window kernel
+    // (16-byte cp.async staging needs 16-byte aligned input rows)
+    const bool al16 = ((uintptr_t)r.U_in & 15) == 0 && (r.ld_in & 1) == 0;
+    const int sepnb = L->sl2d_separable && al16 ? sep_rows(L->n_x, r.B) : 0;
+    const int64_t ptiles = sepnb ? n / ((int64_t)kNT2 * kSepSub) : strip ? n / ((int64_t)kNT2 * nb) : tiles;
     const int64_t need = (V ? 8 * r.B * n : 0) + (partial ? 8 * r.B * ptiles : 0);
     if (need > scratch_bytes) return MGRIT_EINVAL;
     const dim3 grid((unsigned)tiles, (unsigned)r.B);
@@ -1143,7 +1406,9 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             Rows2D s = a;
             s.out = V;
             s.ld_out = n;
-            if (strip)
+            if (sepnb)
+                launch_sep<P, true>(sepnb, r.B, L, s, st);
+            else if (strip)
                 launch_strip<P, true>(nb, sgrid, L, s, st);
             else if (P == 5 && n % kTile2 == 0)
                 sl2d_kernel<P, true, SL2DMinBlocks<P>::value, true, P == 5><<<grid, kNT2, 0, st>>>(*L, s);
@@ -1157,7 +1422,9 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
         }
         Rows2D s = a;
         s.partial = partial;
-        if (strip) {
+        if (sepnb) {
+            launch_sep<P, false>(sepnb, r.B, L, s, st);
+        } else if (strip) {
             launch_strip<P, false>(nb, sgrid, L, s, st);
         } else if (P == 3 && L->n_x == 512) {
             // p = 3 on the 512-wide mesh (cfg4): the tap rows are immediate

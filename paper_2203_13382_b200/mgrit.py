@@ -225,6 +225,20 @@ class Level:
     # first step whose records/sigma are stored (a time-sharded hierarchy keeps
     # only the steps its rank group works on; 0 = all steps)
     set0: int = 0
+    # 2D: the records are separable (s_x independent of the mesh row, s_y of the
+    # column, bitwise), so plain SL steps take the sliding-window kernel
+    # (step2d.cu sl2d_sep_kernel); None = check the records on construction
+    separable: bool | None = None
+
+    def __post_init__(self):
+        if self.separable is None:
+            self.separable = False
+            if self.grid.dim == 2 and self.s_x is not None and self.s_y is not None and self.s_x.is_cuda:
+                flag = torch.zeros(1, dtype=torch.int32, device=self.s_x.device)
+                rc = _lib.load().mgrit_records_separable(self.grid.n_x, self.s_x.shape[0], self.s_x.data_ptr(),
+                                                         self.s_y.data_ptr(), flag.data_ptr(), stream_ptr())
+                _lib.check(rc, "records_separable")
+                self.separable = bool(flag.item())
 
     # -- read-only views of the reference's Level data (mgrit.py:89-117) -----
 
@@ -289,6 +303,7 @@ class Level:
         d.stencil_numba = int(self.stencil_numba if stencil_numba is None else stencil_numba)
         d.gmres_lowsync = int(g.variant == "mgs_lowsync")
         d.launch_policy = LAUNCH_POLICIES[_launch_policy]
+        d.sl2d_separable = int(bool(self.separable))
         return d
 
     @property
