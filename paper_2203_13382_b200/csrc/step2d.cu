@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
     extern __shared__ __align__(16) double s_raw[];   // [cap][kSepW] staged source tile
     __shared__ __align__(16) double s_wy[kSepMaxRows][P + 1];
     __shared__ double s_sy[kSepMaxRows];
-    __shared__ int s_ey[kSepMaxRows];
+    __shared__ int s_ey[kSepMaxRows], s_rk[kSepMaxRows];
     __shared__ int s_cmin[kNT2 / 32], s_cmax[kNT2 / 32];
     __shared__ double red[kNT2 / 32 + 1];
     constexpr int SL = Stencil<P>::L;
@@ -462,6 +462,9 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
     const int span = hi - lo + P + 1;
     const bool staged = allx && rows_ok && span <= cap && width <= kSepW;
 
+    // staged row of each node's first source row
+    if (tid < nb) s_rk[tid] = staged ? rel_of(s_ey[tid]) - lo : 0;
+
     const double *gp = (!SLONLY && a.G) ? a.G + b * a.ld_g + i0 : nullptr;
     const double *up = (!SLONLY && a.U_sub) ? a.U_sub + b * a.ld_sub + i0 : nullptr;
     double *op = a.out ? a.out + b * a.ld_out + i0 : nullptr;
@@ -469,24 +472,38 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
                                               (int64_t)(iy0 / kSepSub) * tiles_x + (ix / kNT2)
                                         : nullptr;
     double ss = 0.0;
-    // output form of node (ix, iy0 + k) (as sl2d_kernel) and the sub-block partials
+    // output form of the column's next node (as sl2d_kernel; called for
+    // k = 0, 1, .. in order: the row pointers advance) and the sub-block partials
     auto emit = [&](int k, double x) {
-        const int64_t ko = (int64_t)k * nx;
         if constexpr (!SLONLY) {
-            const double g = gp ? gp[ko] : 0.0;
-            x = up ? __dsub_rn(__dadd_rn(g, x), up[ko]) : __dadd_rn(x, g);
+            double g = 0.0;
+            if (gp) {
+                g = *gp;
+                gp += nx;
+            }
+            if (up) {
+                x = __dsub_rn(__dadd_rn(g, x), *up);
+                up += nx;
+            } else {
+                x = __dadd_rn(x, g);
+            }
             ss = __dadd_rn(ss, __dmul_rn(x, x));
         }
-        if (op) op[ko] = x;
+        if (op) {
+            *op = x;
+            op += nx;
+        }
         if constexpr (!SLONLY) {
             if (pp && (k & (kSepSub - 1)) == kSepSub - 1) {
                 const double tot = block_sum<kNT2>(ss, red);
-                if (tid == 0) pp[(int64_t)(k / kSepSub) * tiles_x] = tot;
+                if (tid == 0) *pp = tot;
+                pp += tiles_x;
                 ss = 0.0;
             }
         }
     };
     if (!staged) {   // the band's source window does not fit: per-node gathers
+        __syncthreads();
 #pragma unroll 1
         for (int k = 0; k < nb; ++k) emit(k, sl2d_at<P, 0>(u, nx, sx0, s_sy[k]));
         return;
@@ -522,22 +539,32 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
 
-    double W[P + 1];   // row sums of the current node's source rows e - l .. e + r
-    int prev = 0;
-    for (int k = 0; k < nb; ++k) {
-        const int rk = rel_of(s_ey[k]) - lo;   // staged row of the node's first source row
-        int d = rk - prev;
-        if (k == 0 || d < 0 || d > P) d = P + 1;
-        for (int q = d - 1; q >= 0; --q) {     // slide the window down by d rows (uniform over the CTA)
+    // Window of the row sums of source rows rk .. rk + p of the current node.
+    // The slot of source row rk + q rotates with k (slot (k + q) mod (p + 1),
+    // static in the unrolled loop), so the usual one-row slide computes one new
+    // row sum and moves nothing; any other slide recomputes the window.
+    constexpr int Q = P + 1;
+    double W[Q];
+    int prev = -2;
+    for (int k0 = 0; k0 < nb; k0 += Q) {
 #pragma unroll
-            for (int r = 0; r < P; ++r) W[r] = W[r + 1];
-            W[P] = dot(rk + P - q);
+        for (int jj = 0; jj < Q; ++jj) {
+            const int k = k0 + jj;
+            if (k < nb) {
+                const int rk = s_rk[k];
+                if (rk - prev == 1) {
+                    W[(jj + P) % Q] = dot(rk + P);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) W[(jj + q) % Q] = dot(rk + q);
+                }
+                prev = rk;
+                double o = 0.0;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) o = __dadd_rn(o, __dmul_rn(s_wy[k][q], W[(jj + q) % Q]));
+                emit(k, o);
+            }
         }
-        prev = rk;
-        double o = 0.0;
-#pragma unroll
-        for (int q = 0; q <= P; ++q) o = __dadd_rn(o, __dmul_rn(s_wy[k][q], W[q]));
-        emit(k, o);
     }
 }
 
