@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
     __shared__ __align__(16) double s_wy[kSepMaxRows][P + 1];
     __shared__ double s_sy[kSepMaxRows];
     __shared__ int s_ey[kSepMaxRows], s_rk[kSepMaxRows];
-    __shared__ int s_cmin[kNT2 / 32], s_cmax[kNT2 / 32];
+    __shared__ int s_cmin[kNT2 / 32], s_cmax[kNT2 / 32], s_win[3];
     __shared__ double red[kNT2 / 32 + 1];
     constexpr int SL = Stencil<P>::L;
     const int nx = L.n_x;
@@ -407,17 +407,36 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
     const int64_t i0 = (int64_t)iy0 * nx + ix;
     const double *u = a.U_in + b * a.ld_in;
 
-    // column ix's x-record (mesh row 0) and mesh row k's y-record (column 0)
+    // column ix's x-record (mesh row 0); mesh row k's y-record (column 0), its
+    // east row and weights, and the band's source-row window (warp 0: lane k
+    // owns mesh row k): east rows relative to the first one (periodic, nearest
+    // image), lowest row and span
     const double sx0 = __ldg(L.s_x + set * n + ix);
-    if (tid < nb) {
-        const double s = __ldg(L.s_y + set * n + (int64_t)(iy0 + tid) * nx);
-        const Dec d = decompose_s(s, nx);
-        double w[P + 1];
-        lagrange_weights<P>(d.eps, w);
-        s_sy[tid] = s;
-        s_ey[tid] = (unsigned)d.e < (unsigned)nx ? d.e : -1;
+    if (warp == 0) {
+        const bool act = lane < nb;
+        int e = -1;
+        if (act) {
+            const double s = __ldg(L.s_y + set * n + (int64_t)(iy0 + lane) * nx);
+            const Dec d = decompose_s(s, nx);
+            double w[P + 1];
+            lagrange_weights<P>(d.eps, w);
+            s_sy[lane] = s;
+            e = (unsigned)d.e < (unsigned)nx ? d.e : -1;
 #pragma unroll
-        for (int q = 0; q <= P; ++q) s_wy[tid][q] = w[q];
+            for (int q = 0; q <= P; ++q) s_wy[lane][q] = w[q];
+        }
+        const int e0 = __shfl_sync(0xffffffffu, e, 0);
+        int r = act ? e - e0 : 0;
+        if (2 * r < -nx) r += nx;
+        if (2 * r > nx) r -= nx;
+        const int lo = __reduce_min_sync(0xffffffffu, r), hi = __reduce_max_sync(0xffffffffu, r);
+        const bool ok = __all_sync(0xffffffffu, !act || e >= 0);
+        if (act) s_rk[lane] = r - lo;   // staged row of the node's first source row
+        if (lane == 0) {
+            s_win[0] = hi - lo + P + 1;   // span
+            s_win[1] = e0 + lo - SL;      // first source row, in (-nx, 2 nx)
+            s_win[2] = ok;
+        }
     }
     const Dec dx = decompose_s(sx0, nx);
     const bool xok = (unsigned)dx.e < (unsigned)nx;
@@ -441,29 +460,8 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
     }
     const int colbase = cmin & ~1;                 // even: 16-byte aligned copies
     const int width = cmax + P + 1 - colbase;      // staged columns
-    // source-row window of the band: east rows relative to the first one
-    // (periodic, nearest image), first row and span
-    const int e_first = s_ey[0];
-    auto rel_of = [&](int e) {
-        int r = e - e_first;
-        if (2 * r < -nx) r += nx;
-        if (2 * r > nx) r -= nx;
-        return r;
-    };
-    int lo = 0, hi = 0;
-    bool rows_ok = true;
-    for (int k = 0; k < nb; ++k) {
-        const int e = s_ey[k];
-        rows_ok = rows_ok && e >= 0;
-        const int r = rel_of(e);
-        lo = r < lo ? r : lo;
-        hi = r > hi ? r : hi;
-    }
-    const int span = hi - lo + P + 1;
-    const bool staged = allx && rows_ok && span <= cap && width <= kSepW;
-
-    // staged row of each node's first source row
-    if (tid < nb) s_rk[tid] = staged ? rel_of(s_ey[tid]) - lo : 0;
+    const int span = s_win[0];
+    const bool staged = allx && s_win[2] && span <= cap && width <= kSepW;
 
     const double *gp = (!SLONLY && a.G) ? a.G + b * a.ld_g + i0 : nullptr;
     const double *up = (!SLONLY && a.U_sub) ? a.U_sub + b * a.ld_sub + i0 : nullptr;
@@ -473,15 +471,16 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
                                         : nullptr;
     double ss = 0.0;
     // output form of the column's next node (as sl2d_kernel; called for
-    // k = 0, 1, .. in order: the row pointers advance) and the sub-block partials
-    auto emit = [&](int k, double x) {
+    // k = 0, 1, .. in order: the row pointers advance) and the sub-block
+    // partials.  HG / HS: a forcing row / a row to subtract is present.
+    auto emit = [&](auto HG, auto HS, int k, double x) {
         if constexpr (!SLONLY) {
             double g = 0.0;
-            if (gp) {
+            if constexpr (decltype(HG)::value) {
                 g = *gp;
                 gp += nx;
             }
-            if (up) {
+            if constexpr (decltype(HS)::value) {
                 x = __dsub_rn(__dadd_rn(g, x), *up);
                 up += nx;
             } else {
@@ -502,26 +501,37 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
             }
         }
     };
+    // run f(HG, HS) with the output form as compile-time flags
+    auto with_form = [&](auto &&f) {
+        using T = std::true_type;
+        using F = std::false_type;
+        if (gp) {
+            if (up) f(T{}, T{}); else f(T{}, F{});
+        } else {
+            if (up) f(F{}, T{}); else f(F{}, F{});
+        }
+    };
     if (!staged) {   // the band's source window does not fit: per-node gathers
-        __syncthreads();
+        with_form([&](auto HG, auto HS) {
 #pragma unroll 1
-        for (int k = 0; k < nb; ++k) emit(k, sl2d_at<P, 0>(u, nx, sx0, s_sy[k]));
+            for (int k = 0; k < nb; ++k) emit(HG, HS, k, sl2d_at<P, 0>(u, nx, sx0, s_sy[k]));
+        });
         return;
     }
 
     // stage rows [first, first + span) x columns [colbase, colbase + width) (periodic)
     {
-        int first = e_first + lo - SL;
+        int first = s_win[1];
         first = first < 0 ? first + nx : (first >= nx ? first - nx : first);
         const int wch = (width + 1) >> 1;   // 16-byte chunks per row
-        for (int r = warp; r < span; r += kNT2 / 32) {
-            const int row = first + r >= nx ? first + r - nx : first + r;
-            const double *src = u + (int64_t)row * nx;
-            double *dst = s_raw + r * kSepW;
-            for (int c = lane; c < wch; c += 32) {
-                int col = colbase + 2 * c;
-                col = col < 0 ? col + nx : (col >= nx ? col - nx : col);
-                cp_async16(dst + 2 * c, src + col);
+        for (int c = lane; c < wch; c += 32) {
+            int col = colbase + 2 * c;
+            col = col < 0 ? col + nx : (col >= nx ? col - nx : col);
+            const double *src = u + col;
+            double *dst = s_raw + 2 * c;
+            for (int r = warp; r < span; r += kNT2 / 32) {
+                const int row = first + r >= nx ? first + r - nx : first + r;
+                cp_async16(dst + r * kSepW, src + (int64_t)row * nx);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -543,29 +553,35 @@ __global__ void __launch_bounds__(kNT2, 4) sl2d_sep_kernel(mgrit_level_desc L, R
     // The slot of source row rk + q rotates with k (slot (k + q) mod (p + 1),
     // static in the unrolled loop), so the usual one-row slide computes one new
     // row sum and moves nothing; any other slide recomputes the window.
-    constexpr int Q = P + 1;
-    double W[Q];
-    int prev = -2;
-    for (int k0 = 0; k0 < nb; k0 += Q) {
+    with_form([&](auto HG, auto HS) {
+        constexpr int Q = P + 1;
+        double W[Q];
+        int prev = -2;
+        for (int k0 = 0; k0 < nb; k0 += Q) {
 #pragma unroll
-        for (int jj = 0; jj < Q; ++jj) {
-            const int k = k0 + jj;
-            if (k < nb) {
-                const int rk = s_rk[k];
-                if (rk - prev == 1) {
-                    W[(jj + P) % Q] = dot(rk + P);
-                } else {
+            for (int jj = 0; jj < Q; ++jj) {
+                const int k = k0 + jj;
+                if (k < nb) {
+                    const int rk = s_rk[k];
+                    if (rk - prev == 1) {
+                        W[(jj + P) % Q] = dot(rk + P);
+                    } else {
+#pragma unroll 1
+                        for (int q = 0; q < Q; ++q) {   // rare: rebuild the window, oldest row first
 #pragma unroll
-                    for (int q = 0; q < Q; ++q) W[(jj + q) % Q] = dot(rk + q);
+                            for (int r = 0; r < P; ++r) W[(jj + r) % Q] = W[(jj + r + 1) % Q];
+                            W[(jj + P) % Q] = dot(rk + q);
+                        }
+                    }
+                    prev = rk;
+                    double o = 0.0;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) o = __dadd_rn(o, __dmul_rn(s_wy[k][q], W[(jj + q) % Q]));
+                    emit(HG, HS, k, o);
                 }
-                prev = rk;
-                double o = 0.0;
-#pragma unroll
-                for (int q = 0; q < Q; ++q) o = __dadd_rn(o, __dmul_rn(s_wy[k][q], W[(jj + q) % Q]));
-                emit(k, o);
             }
         }
-    }
+    });
 }
 
 // rows per CTA of sl2d_sep_kernel: 16 (a 48 KB table, four CTAs per SM), or 8
