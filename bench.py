@@ -228,9 +228,16 @@ def phase_bytes(level, phase, fine: bool) -> int:
     g = 0 if fine else 1           # G rows read (zero forcing on the fine level)
     d = level.grid.dim             # departure record and sigma: one fp64 per node per axis
     sig = d if level.kind != "fine" and level.sig_x is not None else 0
-    step = 8 * n * (d + g + sig + 1)   # s + G + sigma + output row
+    # departure records: 8 B per node and axis, or one x-record per column and
+    # one y-record per row (noise) on a separable plain-SL 2D level
+    rec = 0 if (d == 2 and level.separable and level.kind in ("fine", "rediscretized")) else d
+    # 2D steps are one batched launch per F-point offset: each step's input row
+    # was written a whole batch (GBs) earlier and is read back from HBM; the 1D
+    # phase kernels carry the row through an interval on chip
+    inp = 1 if d == 2 else 0
+    step = 8 * n * (rec + g + sig + inp + 1)   # s + G + sigma [+ input row] + output row
     if phase == _lib.PHASE_FC:
-        left = 0 if not fine else 8 * n
+        left = 0 if (not fine or inp) else 8 * n
         return nI * (left + m * step)
     if phase == _lib.PHASE_F_RES:
         per = 8 * n * 2 + (m - 1) * step + 8 * n * (d + g + sig) + 8 * n * 3   # tail: s,G,sig + Cbuf r, U w, Gc w
@@ -462,7 +469,8 @@ def _rooflines(args, cfg, levels, breakdown, clk_summary):
     peak = _peak()
     achieved = tb["bytes"] / (tb["ms_avg"] / 1e3) / 1e9
     if "corrected" not in top:
-        limiter = "FP64 issue + L1 gather wavefronts (DESIGN.md section 4)"
+        limiter = ("instruction issue of the separable SL step (DESIGN.md section 4)" if cfg.dim == 2 and levels[0].separable
+                   else "FP64 issue + L1 gather wavefronts (DESIGN.md section 4)")
     elif cfg.dim == 1:
         limiter = "latency: MGS-GMRES reduction chain of a few row chains (see DESIGN.md section 4)"
     else:
@@ -475,7 +483,7 @@ def _rooflines(args, cfg, levels, breakdown, clk_summary):
                 "share_of_iteration": round(tb["ms_avg"] * tb["launches"] / total, 3),
                 "timing": "CUDA events on the launching stream around a graph replay of the phase, "
                           "state restored to the first V-cycle's before each replay"}
-    ops = _ncu_fp64(cfg.dim, cfg.p)
+    ops = _ncu_fp64(cfg.dim, cfg.p, cfg.dim == 2 and bool(levels[0].separable))
     sm_mhz = clk_summary.get("sm_mhz") or 1965.0
     fpeak = 148 * 64 * sm_mhz * 1e6 / 1e12
     if "corrected" not in top and ops:
@@ -507,7 +515,11 @@ def _rooflines(args, cfg, levels, breakdown, clk_summary):
         sl_roof = {"bound": "hbm", "kernel": sl_key, "achieved": round(ach, 1), "peak": peak["hbm_gbs"],
                    "unit": "GB/s", "frac": round(hbm_frac, 4), "traffic": _ncu_traffic(args.config, sl_key),
                    "bytes_per_launch": sb["bytes"], "ms_per_launch": round(sb["ms_avg"], 5),
-                   "note": "plain SL steps of the fine level (8 B record per axis + 8 B new row per node-update)"}
+                   "note": ("plain SL steps of the fine level on separable records: 8 B input row + 8 B new row "
+                            "per node-update (one x-record per column and one y-record per row)")
+                   if (cfg.dim == 2 and levels[0].separable) else
+                   "plain SL steps of the fine level (8 B record per axis + 8 B new row per node-update"
+                   + (" + 8 B input row)" if cfg.dim == 2 else ")")}
         if ops:
             lv0 = levels[0]
             node_updates = lv0.n_steps * lv0.grid.n_points
@@ -660,13 +672,14 @@ def _peak():
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def _ncu_fp64(dim, p):
+def _ncu_fp64(dim, p, separable=False):
     """FP64 instructions per node-update of the fine SL kernel (ncu-measured)."""
     path = os.path.join(ROOT, "profiles", "ncu_fp64.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
-        return json.load(f).get(f"{dim}d_p{p}")
+        d = json.load(f)
+    return d.get(f"{dim}d_p{p}_sep" if separable else f"{dim}d_p{p}", d.get(f"{dim}d_p{p}"))
 
 
 def _ncu_traffic(config, kernel_key):
