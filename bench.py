@@ -215,7 +215,7 @@ class ClockSampler:
 # algorithmic bytes of the fused phase kernels
 
 
-def phase_bytes(level, phase, fine: bool) -> int:
+def phase_bytes(level, phase, fine: bool, c_only: bool = False) -> int:
     """Minimal HBM bytes one launch of a fused phase kernel must move.
 
     8 B per node for every state row read/written, every departure record
@@ -238,6 +238,8 @@ def phase_bytes(level, phase, fine: bool) -> int:
     step = 8 * n * (rec + g + sig + inp + 1)   # s + G + sigma [+ input row] + output row
     if phase == _lib.PHASE_FC:
         left = 0 if (not fine or inp) else 8 * n
+        if c_only:   # the fine 2D FC phase runs only its C-step (mgrit._FusedCycle.skip_f)
+            return nI * step
         return nI * (left + m * step)
     if phase == _lib.PHASE_F_RES:
         per = 8 * n * 2 + (m - 1) * step + 8 * n * (d + g + sig) + 8 * n * 3   # tail: s,G,sig + Cbuf r, U w, Gc w
@@ -488,7 +490,8 @@ def _rooflines(args, cfg, levels, breakdown, clk_summary):
     fpeak = 148 * 64 * sm_mhz * 1e6 / 1e12
     if "corrected" not in top and ops:
         lv0 = levels[0]
-        fach = ops * lv0.n_steps * lv0.grid.n_points / (tb["ms_avg"] / 1e3) / 1e12
+        steps_top = lv0.n_steps // lv0.cf if tb.get("c_only") else lv0.n_steps
+        fach = ops * steps_top * lv0.grid.n_points / (tb["ms_avg"] / 1e3) / 1e12
         roofline["fp64"] = {"achieved": round(fach, 2), "peak": round(fpeak, 2), "unit": "T FP64 inst/s",
                             "frac": round(fach / fpeak, 4), "ops_per_node_update": ops}
     if "corrected" in top and cfg.dim == 1 and "sweep" not in top:
@@ -522,7 +525,7 @@ def _rooflines(args, cfg, levels, breakdown, clk_summary):
                    + (" + 8 B input row)" if cfg.dim == 2 else ")")}
         if ops:
             lv0 = levels[0]
-            node_updates = lv0.n_steps * lv0.grid.n_points
+            node_updates = (lv0.n_steps // lv0.cf if sb.get("c_only") else lv0.n_steps) * lv0.grid.n_points
             fach = ops * node_updates / (sb["ms_avg"] / 1e3) / 1e12
             sl_roof["fp64"] = {"achieved": round(fach, 2), "peak": round(fpeak, 2), "unit": "T FP64 inst/s",
                                "frac": round(fach / fpeak, 4), "ops_per_node_update": ops,
@@ -547,6 +550,7 @@ def kernel_breakdown(levels, cfg, reps: int = 3):
     U = eng.U[0]
     U[0] = M._initial_row(cfg, levels[0], dev)
     M.pcg64_uniform(cfg.seed, cfg.n_t, levels[0].grid.n_points, U[1:], pm1=(cfg.iterate == "pm1"))
+    eng.prologue()   # as solve() does: 2D fine F-points relaxed once, before the first V-cycle
     state = [t for t in list(eng.U) + list(eng.G) + list(eng.C) + [eng.partial] if t is not None]
     torch.cuda.synchronize()
     names = {_lib.PHASE_FC: "FC", _lib.PHASE_F_RES: "F_RES", _lib.PHASE_FONLY_RES: "FONLY_RES",
@@ -560,7 +564,8 @@ def kernel_breakdown(levels, cfg, reps: int = 3):
         seq = [_lib.PHASE_FC, _lib.PHASE_F_RES] if eng.relaxation == "FCF" else [_lib.PHASE_FONLY_RES]
         for ph in seq:
             order.append((f"L{li}_{names[ph]}_{levels[li].kind}", lambda li=li, ph=ph: eng._phase(li, ph),
-                          phase_bytes(levels[li], ph, li == 0)))
+                          phase_bytes(levels[li], ph, li == 0,
+                                      c_only=(li == 0 and ph == _lib.PHASE_FC and eng.skip_f))))
         walk(li + 1)
         ph = _lib.PHASE_INJ_F
         order.append((f"L{li}_{names[ph]}_{levels[li].kind}", lambda li=li, ph=ph: eng._phase(li, ph),
@@ -589,7 +594,8 @@ def kernel_breakdown(levels, cfg, reps: int = 3):
                 ts.append(a.elapsed_time(b))
         del snap, g
         ms = float(np.median(ts))
-        o = out.setdefault(key, {"ms_avg": ms, "bytes": nbytes, "launches": 0})
+        o = out.setdefault(key, {"ms_avg": ms, "bytes": nbytes, "launches": 0,
+                                 "c_only": bool(key.startswith("L0_FC") and eng.skip_f)})
         o["launches"] += 1
     return out
 

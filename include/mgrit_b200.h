@@ -214,7 +214,13 @@ typedef struct mgrit_phase_args {
     double *Cbuf; const double *Uc; double *Gc; int64_t c_row0;
     double *partial; int64_t partial0;
     int32_t zero_init;
-    int32_t pad;
+    int32_t f_relaxed;          /* MGRIT_PHASE_FC on a 2D level: 1 = the F-points already
+                                   hold the F-relaxation of the current C-points (the
+                                   previous V-cycle ended with it, mgrit.py:334, and
+                                   nothing changed since), so the phase runs only its
+                                   C-step; the skipped F-steps would rewrite the same
+                                   bits.  The 1D phase kernels ignore it (they carry the
+                                   interval through shared memory anyway). */
 } mgrit_phase_args;
 
 int mgrit_level_phase(const mgrit_level_desc *L, const mgrit_phase_args *A,

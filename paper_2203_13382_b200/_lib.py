@@ -45,7 +45,7 @@ class PhaseArgs(ctypes.Structure):
         ("G", c_vp), ("ldg", c_i64), ("g_row0", c_i64),
         ("Cbuf", c_vp), ("Uc", c_vp), ("Gc", c_vp), ("c_row0", c_i64),
         ("partial", c_vp), ("partial0", c_i64),
-        ("zero_init", c_i32), ("pad", c_i32),
+        ("zero_init", c_i32), ("f_relaxed", c_i32),
     ]
 
 

@@ -680,8 +680,7 @@ struct Coop2D {
     double *w2;               // [rows_per_round][n] Arnoldi vector (pong)
     double *part;             // [2][rows_per_round][nwb] reduction partials
     int *flags;               // [rows_per_round][chunks] non-finite rhs
-    unsigned int *bar;        // [rows_per_round][kBarStride] per-system barrier words (zeroed per launch)
-    double *tot;              // [rows_per_round][2] totals published by the last arriver
+    unsigned int *bar;        // [rows_per_round] per-system barrier counters (zeroed per launch)
     int32_t *gmres_iters;
     int32_t *status;
 };
@@ -689,76 +688,8 @@ struct Coop2D {
 struct CoopSmem {
     double cs[kMaxK2], sn[kMaxK2], g[kMaxK2 + 1], y[kMaxK2], H[(kMaxK2 + 1) * kMaxK2];
     double red[kNT2 / 32 + 1];
-    double bcast;
-    int stop, last;
+    int stop;
 };
-
-// Barrier over the `chunks` CTAs of one system slot (all CTAs are co-resident:
-// cooperative launch), with the system-wide reduction folded in.  Arrivals
-// increment a per-slot counter; the LAST CTA to arrive sums the slot's
-// per-warp-block partials in the fixed order (per thread a strided sum, then
-// block_sum) and publishes the total and a release flag on a separate cache
-// line; the other CTAs poll that flag (with back-off) and read one double.
-// Polls therefore never queue in front of arrivals on the counter's line, and
-// the partials are read once per barrier instead of once per CTA (on cfg5:
-// 32 KB instead of 296 x 32 KB).  Slots never wait for each other.
-constexpr int kBarStride = 64;   // unsigned words per slot: [0] arrivals, [32] release flag
-struct SysBar {
-    unsigned int *ctr, *flag;
-    double *tot;        // [2] published totals (ping-pong)
-    unsigned int gen;
-    unsigned int chunks;
-};
-
-__device__ __forceinline__ bool sysbar_arrive(SysBar &B) {
-    ++B.gen;
-    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> ctr(*B.ctr);
-    return ctr.fetch_add(1u, cuda::memory_order_acq_rel) + 1u == B.gen * B.chunks;
-}
-__device__ __forceinline__ void sysbar_release(SysBar &B) {
-    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> flag(*B.flag);
-    flag.store(B.gen, cuda::memory_order_release);
-}
-__device__ __forceinline__ void sysbar_wait(SysBar &B) {
-    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> flag(*B.flag);
-    while (flag.load(cuda::memory_order_acquire) < B.gen) __nanosleep(40);
-}
-// plain barrier
-__device__ __forceinline__ void sys_sync(SysBar &B) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (sysbar_arrive(B))
-            sysbar_release(B);
-        else
-            sysbar_wait(B);
-    }
-    __syncthreads();
-}
-// barrier + fixed-order total of pb[0 .. nwb); identical value in every thread of every CTA
-__device__ __forceinline__ double sys_total(SysBar &B, const double *pb, int64_t nwb, int pbuf, CoopSmem &S) {
-    const int tid = threadIdx.x;
-    __syncthreads();
-    if (tid == 0) S.last = sysbar_arrive(B);
-    __syncthreads();
-    double tot;
-    if (S.last) {
-        double acc = 0.0;
-        for (int64_t q = tid; q < nwb; q += kNT2) acc = __dadd_rn(acc, pb[q]);
-        tot = block_sum<kNT2>(acc, S.red);
-        if (tid == 0) {
-            B.tot[pbuf] = tot;
-            sysbar_release(B);
-        }
-    } else {
-        if (tid == 0) {
-            sysbar_wait(B);
-            S.bcast = *(volatile const double *)(B.tot + pbuf);
-        }
-        __syncthreads();
-        tot = S.bcast;
-    }
-    return tot;
-}
 
 template <int P, int NX = 0>
 __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
@@ -835,15 +766,31 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             if (lane == 0 && active_cta) pb[wb] = acc;
         }
     };
-    // per-slot barrier with the reduction folded in (SysBar above); gen is
-    // tracked by thread 0, the only thread that touches the barrier words
-    SysBar SB{C.bar + (int64_t)slot * kBarStride, C.bar + (int64_t)slot * kBarStride + 32, C.tot + 2 * (int64_t)slot, 0u,
-              (unsigned int)C.chunks};
-    auto ssync = [&]() { sys_sync(SB); };
+    // Barrier over the `chunks` CTAs of this system slot only (all CTAs are
+    // co-resident: cooperative launch).  Monotonic per-slot counter, release
+    // on arrival, acquire on the spin (which also invalidates stale L1
+    // lines), so slots never wait for each other: a system that converges
+    // early frees HBM bandwidth for the rest instead of idling in lock-step.
+    unsigned int gen = 0;
+    auto ssync = [&]() {
+        __syncthreads();
+        if (tid == 0) {
+            ++gen;
+            cuda::atomic_ref<unsigned int, cuda::thread_scope_device> ctr(C.bar[slot]);
+            ctr.fetch_add(1u, cuda::memory_order_release);
+            const unsigned int target = gen * (unsigned int)C.chunks;
+            while (ctr.load(cuda::memory_order_acquire) < target) {
+            }
+        }
+        __syncthreads();
+    };
     // system barrier, then the fixed-order total of the system's partials
     auto gtotal = [&]() -> double {
+        ssync();
         const double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
-        const double tot = sys_total(SB, pb, nwb, pbuf, S);
+        double acc = 0.0;
+        for (int64_t q = tid; q < nwb; q += kNT2) acc = __dadd_rn(acc, pb[q]);
+        const double tot = block_sum<kNT2>(acc, S.red);
         pbuf ^= 1;
         return tot;
     };
@@ -1337,8 +1284,7 @@ static int64_t coop_row_bytes(const mgrit_level_desc *L) {
     const int64_t n = L->n_points, nwb = (n + kWB - 1) / kWB;
     // basis (K+1) + two Arnoldi vectors, the reduction partials (two banks for
     // the classic loop, 2K+2 arrays for the low-sync one), flags, barrier word
-    // ... and per system 2 published totals + kBarStride barrier words (256-byte aligned)
-    return 8 * ((int64_t)(L->gmres_max_iters + 3) * n + (int64_t)kLsVals * nwb) + 4 * 4096 + 16 + 4 * kBarStride + 512;
+    return 8 * ((int64_t)(L->gmres_max_iters + 3) * n + (int64_t)kLsVals * nwb) + 4 * 4096 + 8;
 }
 
 int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows) {
@@ -1460,10 +1406,8 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             C.w2 = C.w + rows * n;
             C.part = C.w2 + rows * n;
             C.flags = (int *)(C.part + (int64_t)kLsVals * rows * nwb);
-            C.tot = (double *)(((uintptr_t)(C.flags + rows * chunks) + 255) & ~(uintptr_t)255);
-            C.bar = (unsigned int *)(C.tot + 2 * rows);
-            C.bar = (unsigned int *)(((uintptr_t)C.bar + 255) & ~(uintptr_t)255);
-            if (cudaMemsetAsync(C.bar, 0, rows * kBarStride * sizeof(unsigned int), st) != cudaSuccess) {
+            C.bar = (unsigned int *)(C.flags + rows * chunks);
+            if (cudaMemsetAsync(C.bar, 0, rows * sizeof(unsigned int), st) != cudaSuccess) {
                 set_error("cudaMemsetAsync", cudaGetLastError());
                 return (int)MGRIT_ECUDA;
             }
@@ -1601,9 +1545,11 @@ int level_phase_2d(const mgrit_level_desc *L, const mgrit_phase_args *A, void *s
         // rank's copy, so the C-point residual of its last interval is current)
         if ((rc = axpy_rows_impl(Urow(cb * m), A->ldu, m, Ucrow(cb), n, cnt + 1, n, st))) return rc;
     }
-    // ---- F-relaxation
-    for (int64_t k = 1; k < m; ++k)
-        if ((rc = steps(k, Urow(cb * m + k), ldm, nullptr, 0, nullptr))) return rc;
+    // ---- F-relaxation (skipped by an FC phase whose F-points are known to
+    // hold it already: the steps would rewrite identical rows)
+    if (!(phase == MGRIT_PHASE_FC && A->f_relaxed && !A->zero_init))
+        for (int64_t k = 1; k < m; ++k)
+            if ((rc = steps(k, Urow(cb * m + k), ldm, nullptr, 0, nullptr))) return rc;
     // ---- tails
     if (phase == MGRIT_PHASE_FC) {
         RowsArgs r{cnt, nullptr, cb * m + m - 1, m, Urow(cb * m + m - 1), ldm, Grow(cb * m + m), ldgm,

@@ -673,6 +673,16 @@ class _FusedCycle:
         for li in range(L - 1):
             for ph in (_lib.PHASE_FC, _lib.PHASE_F_RES, _lib.PHASE_FONLY_RES, _lib.PHASE_INJ_F):
                 self._args[(li, ph)] = self._make_args(li, ph)
+        # The reference's V-cycle ends with an F-relaxation of the fine level
+        # (mgrit.py:334) and the next one starts with the same F-relaxation
+        # (mgrit.py:325) of unchanged C-points: identical rows.  On 2D levels
+        # (one batched launch per F-point offset) the fine FC phase therefore
+        # runs only its C-step; prologue() establishes the invariant before the
+        # first V-cycle.  (1D phase kernels walk the interval on chip anyway.)
+        self.skip_f = levels[0].grid.dim == 2 and relaxation == "FCF" and L > 1
+        if self.skip_f:
+            self._fc_full = self._make_args(0, _lib.PHASE_FC)
+            self._args[(0, _lib.PHASE_FC)].f_relaxed = 1
 
     def _make_args(self, li, phase):
         lv = self.levels[li]
@@ -700,6 +710,15 @@ class _FusedCycle:
                                    self.scratch.data_ptr(), self.scratch.numel(), self.status.data_ptr(),
                                    stream_ptr())
         _lib.check(rc, "level_phase")
+
+    def prologue(self):
+        """F-relax the fine level once before the first V-cycle (see skip_f)."""
+        if self.skip_f:
+            lib = _lib.load()
+            rc = lib.mgrit_level_phase(ctypes.byref(self.descs[0]), ctypes.byref(self._fc_full),
+                                       self.scratch.data_ptr(), self.scratch.numel(), self.status.data_ptr(),
+                                       stream_ptr())
+            _lib.check(rc, "level_phase")
 
     def cycle(self, li: int = 0):
         if li == len(self.levels) - 1:
@@ -778,6 +797,8 @@ def solve(cfg: SolverConfig, levels: list[Level] | None = None, *, initial_itera
     state = "max_iters"
     G0 = torch.zeros_like(U) if not use_fused else None
 
+    if use_fused and cfg.max_iters >= 1:
+        sess.engine.prologue()
     if use_fused and use_graph and cfg.max_iters >= 1:
         # device-resident loop: one graph launch, one host sync per solve
         loop = _solve_loop(sess, cfg, status)

@@ -181,3 +181,27 @@ def test_sep_production_meshes_bitwise(P, sep_rows):
         got = _np(fine.step_batch(np.array(steps), torch.from_numpy(U).cuda()))
         for b, t in enumerate(steps):
             assert np.array_equal(got[b], ol.step(t, U[b])), (n_x, t)
+
+
+def test_fine_fc_phase_skips_redundant_f_relaxation_bitwise(P):
+    """2D solves run the fine FC phase without its F-steps (the previous
+    V-cycle's closing F-relaxation, mgrit.py:334, already produced those
+    rows; _FusedCycle.prologue covers the first cycle).  Iterates and
+    histories are bit-identical to the engine that repeats them."""
+    from paper_2203_13382_b200 import _lib, mgrit as M
+    kw = dict(n_x=256, n_t=64, dim=2, wave_speed="B4", p=3, schedule=4, seed=3, u0="sin4", max_iters=4, rtol=0.0)
+    cfg = P.SolverConfig(**kw)
+    levels = P.build_hierarchy(cfg)
+    outs = []
+    for skip in (True, False):
+        levels[0].__dict__.pop("_sessions", None)
+        sess = M._session(levels, cfg, torch.device("cuda"))
+        assert sess.engine.skip_f
+        if not skip:
+            sess.engine.skip_f = False
+            sess.engine._args[(0, _lib.PHASE_FC)].f_relaxed = 0
+        rep, U = P.solve(cfg, levels, output="device", use_graph=skip)
+        outs.append((rep.residual_norms.copy(), U.clone()))
+    levels[0].__dict__.pop("_sessions", None)
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])

@@ -21,6 +21,7 @@ U = torch.empty((cfg.n_t + 1, n), dtype=torch.float64, device="cuda")
 U[0] = torch.from_numpy(M.initial_state(cfg, levels[0].grid)).cuda()
 M.pcg64_uniform(cfg.seed, cfg.n_t, n, U[1:])
 eng = M._FusedCycle(levels, U, cfg.relaxation)
+eng.prologue()
 eng.iteration()
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
