@@ -392,12 +392,12 @@ def run_gpu(args):
         return
     clk_summary = clk.summary()
     roofline = sl_roof = breakdown = None
-    seq = None
+    seq = seq_forms = None
     if world == 1:
         # ---- per-launch breakdown of the first V-cycle (CUDA graphs, events)
         breakdown = kernel_breakdown(levels, cfg)
         roofline, sl_roof = _rooflines(args, cfg, levels, breakdown, clk_summary)
-        seq = sequential_gpu(levels, cfg)
+        seq, seq_forms = sequential_gpu(levels, cfg)
     parity = bench_parity(args.config, rep, P)
     iters = rep.iterations
     cpu = None
@@ -426,6 +426,7 @@ def run_gpu(args):
     }
     if seq is not None:
         line["sequential_gpu_ms"] = round(seq, 3)
+        line["sequential_gpu_forms_ms"] = seq_forms
         line["speedup_vs_sequential_gpu"] = round(seq / ms, 4)
     if breakdown is not None:
         line["kernel_breakdown_ms"] = {k: round(v["ms_avg"] * v["launches"], 4) for k, v in breakdown.items()}
@@ -438,9 +439,31 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def sequential_gpu(levels, cfg) -> float:
+def sequential_gpu(levels, cfg):
     """Plain sequential time stepping of the fine level (the sweep behind
-    P.sequential_reference); state buffer and u0 prepared outside the timing."""
+    P.sequential_reference).  1D: the faster of the one-CTA sweep and the
+    cluster-split sweep (the row split over up to 16 SMs, DSMEM/TMA-multicast
+    row publication); returns (best ms, {form: ms})."""
+    import paper_2203_13382_b200 as P
+    if cfg.dim == 2:
+        ms = _sequential_gpu_once(levels, cfg)
+        return ms, {"batched_sl_steps": round(ms, 3)}
+    forms = {}
+    prev = P.set_launch_policy("cta")
+    try:
+        forms["one_cta"] = round(_sequential_gpu_once(levels, cfg), 3)
+        P.set_launch_policy("cluster")
+        try:
+            forms["cluster"] = round(_sequential_gpu_once(levels, cfg), 3)
+        except RuntimeError:
+            pass   # row length not splittable over a cluster
+    finally:
+        P.set_launch_policy(prev)
+    return min(forms.values()), forms
+
+
+def _sequential_gpu_once(levels, cfg) -> float:
+    """One form of the sweep; state buffer and u0 prepared outside the timing."""
     import torch
     from paper_2203_13382_b200 import mgrit as M
     npts = cfg.n_x ** cfg.dim

@@ -59,7 +59,7 @@ int sweep_1d(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G,
              int zero_init, int32_t *gmres_iters, void *scratch, int64_t scratch_bytes,
              int32_t *status, cudaStream_t st) {
     if (int rc = validate(L)) return rc;
-    if (L->kind == MGRIT_KIND_CORRECTED && U) {
+    if ((L->kind == MGRIT_KIND_CORRECTED || L->kind == MGRIT_KIND_SL) && U) {
         const int rc = cl_sweep(L, U, ldu, G, ldg, zero_init, gmres_iters, status, st);
         if (rc >= 0) return rc;
     }

@@ -130,6 +130,17 @@ int cl_sweep(const mgrit_level_desc *L, double *U, int64_t ldu, const double *G,
     // one chain: the size with the cheapest wave
     const int force = forced_cs(L);
     int best_cs = 0, best_w = 0;
+    if (L->kind == MGRIT_KIND_SL) {
+        // plain SL sweep (sequential time stepping of a fine level): only on
+        // request (MGRIT_LAUNCH_CLUSTER*), the largest eligible cluster
+        if (L->launch_policy != MGRIT_LAUNCH_CLUSTER && !force) return -1;
+        for (int cs : kClSizes)
+            if ((!force || cs == force) && cs_eligible(L, cs)) best_cs = cs;
+        if (!best_cs) return -1;
+        return by_p_cs(L->p, best_cs, [&](auto X) {
+            return decltype(X)::sweep(L, U, ldu, G, ldg, zero_init, gmres_iters, status, st);
+        });
+    }
     for (int cs : kClSizes) {
         if (force && cs != force) continue;
         if (!cs_eligible(L, cs)) continue;

@@ -423,6 +423,13 @@ __device__ int cl_apply(const mgrit_level_desc &L, int64_t t, ClCtx<CS> &cx, dou
         }
         v[k] = acc;
     }
+    if (L.kind == MGRIT_KIND_SL) {
+        // plain SL step (the cluster-split sequential sweep of a fine level):
+        // no solve.  Every CTA must be done reading the shared-memory row
+        // before anyone's publish_row multicasts the next one into it.
+        if constexpr (!GG) cluster_sync_all();
+        return 0;
+    }
     const int64_t set = L.shared ? 0 : t;
     const double *sig = L.sig_x + set * (int64_t)n + cx.base;
     // sigma in registers, or re-read (L1) for the widest rows
@@ -871,7 +878,8 @@ inline int cl_npt(int n) {
 
 template <int CS>
 inline bool cl_eligible(const mgrit_level_desc *L) {
-    if (L->kind != MGRIT_KIND_CORRECTED || L->dim != 1) return false;
+    // (plain SL levels: the sequential sweep only, see cl_sweep)
+    if ((L->kind != MGRIT_KIND_CORRECTED && L->kind != MGRIT_KIND_SL) || L->dim != 1) return false;
     if (!cl_npt<CS>(L->n_x)) return false;
     // (16 nodes per thread leave no registers for the low-sync variant;
     //  those launches run classic MGS, see LaunchCl)

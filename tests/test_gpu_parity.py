@@ -442,6 +442,25 @@ def test_sequential_reference_matches_oracle(P):
     assert np.array_equal(U, O.sequential(ocfg, olevels))
 
 
+@pytest.mark.parametrize("policy", ["cluster", "cluster2", "cluster4", "cluster8", "cluster16"])
+@pytest.mark.parametrize("n_x,p", [(1024, 1), (4096, 3), (16384, 5)])
+def test_sequential_reference_cluster_sweep_bitwise(P, policy, n_x, p):
+    """The cluster-split plain-SL sweep (the row split over 2-16 SMs; the
+    strongest sequential GPU baseline bench.py reports) gives the same bits as
+    the one-CTA sweep, which the test above pins to the oracle."""
+    cfg = P.SolverConfig(n_x=n_x, n_t=48, wave_speed="B2", p=p, schedule=4)
+    levels = P.build_hierarchy(cfg)
+    prev = P.set_launch_policy("cta")
+    try:
+        ref = P.sequential_reference(cfg, levels, output="device").clone()
+        P.set_launch_policy(policy)
+        got = P.sequential_reference(cfg, levels, output="device")
+    finally:
+        P.set_launch_policy(prev)
+    assert torch.equal(got, ref)
+    assert float(ref[-1].abs().max()) > 0.0
+
+
 def test_mgrit_converges_to_sequential(P):
     cfg = P.SolverConfig(n_x=64, n_t=256, wave_speed="C3", p=3, schedule=4)
     rep, U = P.solve(cfg)
