@@ -238,8 +238,8 @@ def phase_bytes(level, phase, fine: bool, c_only: bool = False) -> int:
     step = 8 * n * (rec + g + sig + inp + 1)   # s + G + sigma [+ input row] + output row
     if phase == _lib.PHASE_FC:
         left = 0 if (not fine or inp) else 8 * n
-        if c_only:   # the fine 2D FC phase runs only its C-step (mgrit._FusedCycle.skip_f)
-            return nI * step
+        if c_only:   # the fine FC phase runs only its C-step (mgrit._FusedCycle.skip_f)
+            return nI * (step + (0 if inp else 8 * n))   # 1D: the last F row is read back
         return nI * (left + m * step)
     if phase == _lib.PHASE_F_RES:
         per = 8 * n * 2 + (m - 1) * step + 8 * n * (d + g + sig) + 8 * n * 3   # tail: s,G,sig + Cbuf r, U w, Gc w
@@ -532,7 +532,11 @@ def _rooflines(args, cfg, levels, breakdown, clk_summary):
 
     # the SL-step kernel itself (BASELINE: "SL-step HBM GB/s"): the fine-level
     # F+C relaxation phase (plain semi-Lagrangian steps, G = 0)
-    sl_key = next((k for k in breakdown if k.startswith("L0_FC") or k.startswith("L0_FONLY")), None)
+    # 2D: the FC phase (since round 2 exactly one batched SL step of every
+    # interval); 1D: the fused F-relaxation + C-point residual phase (the FC
+    # phase is a small C-step-only row launch there)
+    pref = ("L0_FC", "L0_FONLY") if cfg.dim == 2 else ("L0_F_RES", "L0_FONLY", "L0_FC")
+    sl_key = next((k for pfx in pref for k in breakdown if k.startswith(pfx)), None)
     sl_roof = None
     if sl_key is not None:
         sb = breakdown[sl_key]
@@ -548,7 +552,8 @@ def _rooflines(args, cfg, levels, breakdown, clk_summary):
                    + (" + 8 B input row)" if cfg.dim == 2 else ")")}
         if ops:
             lv0 = levels[0]
-            node_updates = (lv0.n_steps // lv0.cf if sb.get("c_only") else lv0.n_steps) * lv0.grid.n_points
+            node_updates = (lv0.n_steps // lv0.cf if (sb.get("c_only") and sl_key.startswith("L0_FC"))
+                            else lv0.n_steps) * lv0.grid.n_points
             fach = ops * node_updates / (sb["ms_avg"] / 1e3) / 1e12
             sl_roof["fp64"] = {"achieved": round(fach, 2), "peak": round(fpeak, 2), "unit": "T FP64 inst/s",
                                "frac": round(fach / fpeak, 4), "ops_per_node_update": ops,

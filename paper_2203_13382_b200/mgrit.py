@@ -675,11 +675,13 @@ class _FusedCycle:
                 self._args[(li, ph)] = self._make_args(li, ph)
         # The reference's V-cycle ends with an F-relaxation of the fine level
         # (mgrit.py:334) and the next one starts with the same F-relaxation
-        # (mgrit.py:325) of unchanged C-points: identical rows.  On 2D levels
-        # (one batched launch per F-point offset) the fine FC phase therefore
-        # runs only its C-step; prologue() establishes the invariant before the
-        # first V-cycle.  (1D phase kernels walk the interval on chip anyway.)
-        self.skip_f = levels[0].grid.dim == 2 and relaxation == "FCF" and L > 1
+        # (mgrit.py:325) of unchanged C-points: identical rows.  The fine FC
+        # phase therefore runs only its C-step; prologue() establishes the
+        # invariant before the first V-cycle.  2D: the phase launch skips its
+        # batched F-steps (mgrit_phase_args::f_relaxed).  1D: the C-step is one
+        # batched row launch (U[(c+1)m - 1] -> Cbuf[c + 1] for every interval)
+        # instead of the fused phase kernel, which would walk the interval again.
+        self.skip_f = relaxation == "FCF" and L > 1 and levels[0].kind != "ideal"
         if self.skip_f:
             self._fc_full = self._make_args(0, _lib.PHASE_FC)
             self._args[(0, _lib.PHASE_FC)].f_relaxed = 1
@@ -706,6 +708,12 @@ class _FusedCycle:
 
     def _phase(self, li, phase):
         lib = _lib.load()
+        if li == 0 and phase == _lib.PHASE_FC and self.skip_f and self.levels[0].grid.dim == 1:
+            lv = self.levels[0]
+            n, m = lv.grid.n_points, lv.cf
+            U = self.U[0]
+            lv._apply(U[m - 1:], m - 1, m, lv.n_steps // m, self.C[0][1:], ld_in=m * n, ld_out=n)
+            return
         rc = lib.mgrit_level_phase(ctypes.byref(self.descs[li]), ctypes.byref(self._args[(li, phase)]),
                                    self.scratch.data_ptr(), self.scratch.numel(), self.status.data_ptr(),
                                    stream_ptr())

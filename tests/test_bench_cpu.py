@@ -71,3 +71,32 @@ def test_reference_arm_prints_the_gpu_arm_config():
     assert d["impl"] == "reference"
     assert d["config"] == bench.static_config("cfg1")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
+
+
+def test_phase_bytes_2d_counts_input_rows_and_separable_records():
+    """Algorithmic bytes of the fused phases: a 2D
+    batched step reads its input row from HBM (8 B) and writes 8 B; per-node
+    records add 16 B, separable records nothing; the fine 2D FC phase that
+    skips its F-steps is one step per interval.  1D keeps the row on chip."""
+    import types
+
+    import bench
+    from paper_2203_13382_b200 import _lib
+
+    def level(dim, n, steps, m, kind="fine", separable=False, sig=None):
+        grid = types.SimpleNamespace(n_points=n, dim=dim)
+        return types.SimpleNamespace(grid=grid, n_steps=steps, cf=m, kind=kind, separable=separable, sig_x=sig)
+
+    n, N, m = 1 << 20, 2048, 8
+    nI = N // m
+    per_node = bench.phase_bytes(level(2, n, N, m), _lib.PHASE_FC, True)
+    sep = bench.phase_bytes(level(2, n, N, m, separable=True), _lib.PHASE_FC, True)
+    assert per_node == nI * m * 8 * n * 4            # 2 records + input + output
+    assert sep == nI * m * 8 * n * 2                 # input + output
+    assert bench.phase_bytes(level(2, n, N, m, separable=True), _lib.PHASE_FC, True, c_only=True) == nI * 16 * n
+    # a corrected 2D level is never "separable" for the byte count (per-node records + sigma + G)
+    corr = bench.phase_bytes(level(2, n, 256, m, kind="corrected", separable=True, sig=object()), _lib.PHASE_FC, False)
+    assert corr == (256 // m) * m * 8 * n * (2 + 1 + 2 + 1 + 1)
+    # 1D fine level: left C row once per interval, then record + output per step
+    n1 = 4096
+    assert bench.phase_bytes(level(1, n1, 4096, 4), _lib.PHASE_FC, True) == (4096 // 4) * (8 * n1 + 4 * 16 * n1)

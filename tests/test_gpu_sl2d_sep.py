@@ -183,13 +183,20 @@ def test_sep_production_meshes_bitwise(P, sep_rows):
             assert np.array_equal(got[b], ol.step(t, U[b])), (n_x, t)
 
 
-def test_fine_fc_phase_skips_redundant_f_relaxation_bitwise(P):
-    """2D solves run the fine FC phase without its F-steps (the previous
+@pytest.mark.parametrize("kw", [
+    dict(n_x=256, n_t=64, dim=2, wave_speed="B4", p=3, schedule=4, seed=3, u0="sin4"),
+    dict(n_x=4096, n_t=256, wave_speed="B2", p=3, schedule=4, seed=1),
+    dict(n_x=16384, n_t=128, wave_speed="B2", p=5, schedule=8, seed=2),
+    dict(n_x=1024, n_t=128, wave_speed="C1", p=1, schedule=8, max_levels=2, dt=0.85 * 2.0 / 1024),
+], ids=["2d", "1d_n4096", "1d_n16384", "1d_two_level"])
+def test_fine_fc_phase_skips_redundant_f_relaxation_bitwise(P, kw):
+    """Solves run the fine FC phase without its F-steps (the previous
     V-cycle's closing F-relaxation, mgrit.py:334, already produced those
-    rows; _FusedCycle.prologue covers the first cycle).  Iterates and
+    rows; _FusedCycle.prologue covers the first cycle): 2D through
+    mgrit_phase_args::f_relaxed, 1D as one batched row launch.  Iterates and
     histories are bit-identical to the engine that repeats them."""
     from paper_2203_13382_b200 import _lib, mgrit as M
-    kw = dict(n_x=256, n_t=64, dim=2, wave_speed="B4", p=3, schedule=4, seed=3, u0="sin4", max_iters=4, rtol=0.0)
+    kw = dict(kw, max_iters=4, rtol=0.0)
     cfg = P.SolverConfig(**kw)
     levels = P.build_hierarchy(cfg)
     outs = []
