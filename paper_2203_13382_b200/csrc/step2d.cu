@@ -1548,8 +1548,18 @@ int level_phase_2d(const mgrit_level_desc *L, const mgrit_phase_args *A, void *s
     // ---- F-relaxation (skipped by an FC phase whose F-points are known to
     // hold it already: the steps would rewrite identical rows)
     if (!(phase == MGRIT_PHASE_FC && A->f_relaxed && !A->zero_init))
-        for (int64_t k = 1; k < m; ++k)
+        for (int64_t k = 1; k < m; ++k) {
+            if (k == 1 && A->zero_init && (phase == MGRIT_PHASE_FC || phase == MGRIT_PHASE_FONLY_RES) &&
+                L->kind != MGRIT_KIND_FORWARD_EULER) {
+                // the left C rows are zero: Phi 0 = +0.0 (an SL gather of zeros; GMRES returns
+                // x = 0 at beta = 0, _kernels.py:123-128), so the step's row is 0.0 + g
+                if ((rc = zero_rows(Urow(cb * m + 1), ldm, cnt, n, st))) return rc;
+                if (A->G && (rc = axpy_rows_impl(Urow(cb * m + 1), A->ldu, m, Grow(cb * m + 1), ldgm, cnt, n, st)))
+                    return rc;
+                continue;
+            }
             if ((rc = steps(k, Urow(cb * m + k), ldm, nullptr, 0, nullptr))) return rc;
+        }
     // ---- tails
     if (phase == MGRIT_PHASE_FC) {
         RowsArgs r{cnt, nullptr, cb * m + m - 1, m, Urow(cb * m + m - 1), ldm, Grow(cb * m + m), ldgm,
