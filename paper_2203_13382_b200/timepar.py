@@ -168,6 +168,10 @@ def make_plan(sizes: list[int], factors: list[int | None], rank: int, size: int)
 class CudaPhaseBackend:
     """Launches the fused phase kernels / sweep of libmgrit_b200.so."""
 
+    # a 2D FC phase can be told that its F-points are already relaxed
+    # (mgrit_phase_args::f_relaxed); see TimeParallelCycle.skip_f
+    supports_f_relaxed = True
+
     def __init__(self, levels):
         from .mgrit import _WS
         self.levels = levels
@@ -188,7 +192,7 @@ class CudaPhaseBackend:
         return torch.cuda.current_stream().cuda_stream
 
     def phase(self, li, phase, *, m, c_begin, c_count, n_intervals, U, u_row0, G, g_row0, Cbuf, Uc, Gc,
-              c_row0, partial, partial0, zero_init):
+              c_row0, partial, partial0, zero_init, f_relaxed=0):
         a = _lib.PhaseArgs()
         n = self.levels[li].grid.n_points
         a.phase, a.m = phase, m
@@ -202,6 +206,7 @@ class CudaPhaseBackend:
         a.partial = 0 if partial is None else partial.data_ptr()
         a.partial0 = partial0
         a.zero_init = int(zero_init)
+        a.f_relaxed = int(f_relaxed)
         rc = self.lib.mgrit_level_phase(ctypes.byref(self.descs[li]), ctypes.byref(a), self.scratch.data_ptr(),
                                         self.scratch.numel(), self.status.data_ptr(), self._stream())
         _lib.check(rc, "level_phase")
@@ -251,6 +256,18 @@ class TimeParallelCycle:
         self.partial = torch.zeros(p0.ce - p0.cb, dtype=dtype, device=device)
         self.partial_all = torch.zeros(p0.n_intervals, dtype=dtype, device=device)
         self.sumsq = torch.zeros(1, dtype=dtype, device=device)
+        # As in mgrit._FusedCycle: a V-cycle ends with the fine F-relaxation the
+        # next one would start with (same C-points: a rank's F-points depend on
+        # its own left C-points only, the row received from the right neighbour
+        # is an interval's right end), so the fine 2D FC phase runs only its
+        # C-step once prologue() has F-relaxed the rank's intervals.
+        lv = getattr(backend, "levels", None)
+        self.skip_f = bool(getattr(backend, "supports_f_relaxed", False) and relaxation == "FCF" and L > 1
+                           and plans[0].m is not None and lv is not None and lv[0].grid.dim == 2)
+
+    def prologue(self):
+        if self.skip_f:
+            self.be.phase(0, _lib.PHASE_FC, **self._args(0, _lib.PHASE_FC, False))
 
     def _args(self, li, phase, zero_init):
         p, c = self.plans[li], self.plans[li + 1]
@@ -275,7 +292,10 @@ class TimeParallelCycle:
             return
         last_local = p.ce - p.cb
         if self.relax == "FCF":
-            be.phase(li, _lib.PHASE_FC, **self._args(li, _lib.PHASE_FC, zero))
+            if li == 0 and self.skip_f:
+                be.phase(li, _lib.PHASE_FC, f_relaxed=1, **self._args(li, _lib.PHASE_FC, zero))
+            else:
+                be.phase(li, _lib.PHASE_FC, **self._args(li, _lib.PHASE_FC, zero))
             if p.sharded:
                 comm.shift(self.C[li][last_local], self.C[li][0], +1, p.stride)
             be.phase(li, _lib.PHASE_F_RES, **self._args(li, _lib.PHASE_F_RES, zero))
@@ -386,6 +406,7 @@ def solve_time_parallel(cfg, levels, comm: Comm | None = None, *, use_graph: boo
     be.total(row_all, s0)
     r0 = float(torch.sqrt(s0).item())
     eng = TimeParallelCycle(plans, n, be, comm, cfg.relaxation, U, dev)
+    eng.prologue()
     hist, state, graph = [r0], "max_iters", None
     for it in range(cfg.max_iters):
         if graph is not None:

@@ -59,6 +59,7 @@ def per_rank_ms(cfg, levels, rank, size, iters=3):
     comm = StubComm(rank, size)
     be = T.CudaPhaseBackend(levels)
     eng = T.TimeParallelCycle(plans, n, be, comm, cfg.relaxation, U, dev)
+    eng.prologue()
     eng.iteration()
     torch.cuda.synchronize()
     comm.bytes = 0
