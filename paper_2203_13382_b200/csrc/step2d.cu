@@ -28,6 +28,18 @@ namespace mgrit {
 
 namespace {
 
+#ifdef MGRIT_PROBE2D
+// tools/probe_coop2d.cu: per-CTA globaltimer stamps around every system
+// barrier of gmres2d_coop ([cta][2 * barrier]: arrival, release)
+constexpr int kProbeBars = 96;
+__device__ unsigned long long *g_probe2d = nullptr;
+__device__ __forceinline__ unsigned long long probe_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 constexpr int kNT2 = 256;       // threads per CTA for 2D kernels
 constexpr int kTile2 = 1024;    // nodes per CTA tile (4 per thread)
 constexpr int kMaxK2 = 16;
@@ -694,6 +706,7 @@ struct CoopSmem {
 template <int P, int NX = 0>
 __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     __shared__ CoopSmem S;
+    __shared__ double s_tile[(kNT2 / 32) * (32 + (P + 1)) * (kWBPerLane + (P + 1))];   // per warp: a patch + halo
     const mgrit_level_desc &L = C.L;
     const Rows2D &a = C.a;
     const int nx = L.n_x;
@@ -709,57 +722,48 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     constexpr int NW = kNT2 / 32;
     int pbuf = 0;
 
-    // for every node of this CTA's warp blocks: body(i); optional reduction of
-    // red(i) per warp block into the current partial buffer
-    // nx % 256 == 0 (every BASELINE 2D mesh): a warp block lies inside one
-    // grid row, so (ix, iy) come from one division per block
+    // Node mapping of a warp block (256 nodes, 8 per lane), fixed per mesh so
+    // that every reduction's partials and their order are independent of how
+    // many CTAs share a system:
+    //  * patch mode (n_x a multiple of 32: every BASELINE mesh): a 32 x 8 patch,
+    //    lane = column, k = row.  Patches are numbered along x, so a warp still
+    //    reads 256 contiguous bytes per row, and the stencil pass can stage a
+    //    patch plus its halo in shared memory (below);
+    //  * otherwise 256 consecutive nodes, lane + 32 k.
+    const bool patch = (nx % 32) == 0;
+    const int pbx = nx / 32;   // patches per patch row
     const bool row_blocks = (nx % kWB) == 0;
-    auto for_nodes = [&](auto &&body) {
-        for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
-            const int64_t base = wb * kWB;
-            const int iy0 = row_blocks ? (int)(base / nx) : 0;
-            const int ix0 = row_blocks ? (int)(base - (int64_t)iy0 * nx) : 0;
-#pragma unroll
-            for (int k = 0; k < kWBPerLane; ++k) {
-                const int64_t i = base + lane + 32 * k;
-                if (i < n) {
-                    int ix, iy;
-                    if (row_blocks) {
-                        ix = ix0 + lane + 32 * k;
-                        iy = iy0;
-                    } else {
-                        iy = (int)((unsigned)i / (unsigned)nx);
-                        ix = (int)i - iy * nx;
-                    }
-                    body(i, ix, iy);
-                }
-            }
-        }
-    };
-    // for_nodes fused with the per-warp-block reduction of body's return
-    // value: same node -> (lane, k) mapping and the same per-lane order as
-    // reduce_nodes, so the partials are bit-identical to the two-pass form
-    // while the vectors are read once
+    // for every node of this CTA's warp blocks, body(i, ix, iy) -> value; the
+    // per-warp-block sum (per lane in k order, then the butterfly) goes to the
+    // current partial buffer
     auto for_nodes_red = [&](auto &&body) {
         double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
         for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
-            const int64_t base = wb * kWB;
-            const int iy0 = row_blocks ? (int)(base / nx) : 0;
-            const int ix0 = row_blocks ? (int)(base - (int64_t)iy0 * nx) : 0;
             double acc = 0.0;
+            if (patch) {
+                const int by = (int)(wb / pbx);
+                const int ix = ((int)(wb - (int64_t)by * pbx)) * 32 + lane;
+                int64_t i = (int64_t)by * kWBPerLane * nx + ix;
 #pragma unroll
-            for (int k = 0; k < kWBPerLane; ++k) {
-                const int64_t i = base + lane + 32 * k;
-                if (i < n) {
-                    int ix, iy;
-                    if (row_blocks) {
-                        ix = ix0 + lane + 32 * k;
-                        iy = iy0;
-                    } else {
-                        iy = (int)((unsigned)i / (unsigned)nx);
-                        ix = (int)i - iy * nx;
+                for (int k = 0; k < kWBPerLane; ++k, i += nx) acc = __dadd_rn(acc, body(i, ix, by * kWBPerLane + k));
+            } else {
+                const int64_t base = wb * kWB;
+                const int iy0 = row_blocks ? (int)(base / nx) : 0;
+                const int ix0 = row_blocks ? (int)(base - (int64_t)iy0 * nx) : 0;
+#pragma unroll
+                for (int k = 0; k < kWBPerLane; ++k) {
+                    const int64_t i = base + lane + 32 * k;
+                    if (i < n) {
+                        int ix, iy;
+                        if (row_blocks) {
+                            ix = ix0 + lane + 32 * k;
+                            iy = iy0;
+                        } else {
+                            iy = (int)((unsigned)i / (unsigned)nx);
+                            ix = (int)i - iy * nx;
+                        }
+                        acc = __dadd_rn(acc, body(i, ix, iy));
                     }
-                    acc = __dadd_rn(acc, body(i, ix, iy));
                 }
             }
             acc = warp_sum(acc);
@@ -768,19 +772,29 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     };
     // Barrier over the `chunks` CTAs of this system slot only (all CTAs are
     // co-resident: cooperative launch).  Monotonic per-slot counter, release
-    // on arrival, acquire on the spin (which also invalidates stale L1
-    // lines), so slots never wait for each other: a system that converges
+    // on arrival, relaxed polls and one acquire fence at the end (which also
+    // invalidates stale L1 lines), so slots never wait for each other: a system that converges
     // early frees HBM bandwidth for the rest instead of idling in lock-step.
     unsigned int gen = 0;
     auto ssync = [&]() {
         __syncthreads();
         if (tid == 0) {
             ++gen;
+#ifdef MGRIT_PROBE2D
+            if (g_probe2d && gen <= kProbeBars) g_probe2d[((int64_t)blockIdx.x * kProbeBars + gen - 1) * 2] = probe_now();
+#endif
             cuda::atomic_ref<unsigned int, cuda::thread_scope_device> ctr(C.bar[slot]);
             ctr.fetch_add(1u, cuda::memory_order_release);
             const unsigned int target = gen * (unsigned int)C.chunks;
-            while (ctr.load(cuda::memory_order_acquire) < target) {
+            // poll relaxed (every acquire load would invalidate the SM's whole L1,
+            // CCTL.IVALL, under the co-resident CTAs that are still gathering taps);
+            // one acquire fence once the last arrival is seen
+            while (ctr.load(cuda::memory_order_relaxed) < target) {
             }
+            cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+#ifdef MGRIT_PROBE2D
+            if (g_probe2d && gen <= kProbeBars) g_probe2d[((int64_t)blockIdx.x * kProbeBars + gen - 1) * 2 + 1] = probe_now();
+#endif
         }
         __syncthreads();
     };
@@ -842,13 +856,68 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             if (S.stop) break;
             double *bk = basis + (int64_t)kk * n;
             // b_kk, w = A b_kk ; inner product with b_0
-            for_nodes_red([&](int64_t i, int ix, int iy) {
-                double bi;
-                const double x = imsd2d_scaled<P, NX>(src, nx, ix, iy, __ldg(gx + i), __ldg(gy + i), scale, rscale, bi);
-                bk[i] = bi;
-                dst[i] = x;
-                return __dmul_rn(kk == 0 ? bi : basis[i], x);
-            });
+            if (patch) {
+                // Each warp forms b = src / scale ONCE for its patch and a halo of
+                // the stencil radius (shared memory, (32 + 2r) x (8 + 2r) values
+                // for 256 nodes) instead of once per tap (2r(2) + 1 = 13 exact
+                // divisions per node at p = 5); the stencil then reads b from
+                // shared memory.  Same b values, same stencil arithmetic as
+                // imsd2d_scaled: identical w.
+                constexpr int RAD = (P + 1) / 2, TW = 32 + 2 * RAD, TH = kWBPerLane + 2 * RAD;
+                double *T = s_tile + warp * (TW * TH);
+                double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
+                for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
+                    const int by = (int)(wb / pbx);
+                    const int ix0 = ((int)(wb - (int64_t)by * pbx)) * 32, iy0 = by * kWBPerLane;
+                    {
+                        // all of the lane's halo loads in flight at once, then the divisions
+                        constexpr int NT = (TW * TH + 31) / 32;
+                        double v[NT];
+#pragma unroll
+                        for (int jt = 0; jt < NT; ++jt) {
+                            const int t = lane + 32 * jt;
+                            const int hy = t / TW, hx = t - hy * TW;
+                            const int gxx = wrapi(ix0 - RAD + hx, nx), gyy = wrapi(iy0 - RAD + hy, nx);
+                            v[jt] = t < TW * TH ? src[(int64_t)gyy * nx + gxx] : 0.0;
+                        }
+#pragma unroll
+                        for (int jt = 0; jt < NT; ++jt) {
+                            const int t = lane + 32 * jt;
+                            if (t < TW * TH) T[t] = div_rcp(v[jt], scale, rscale);
+                        }
+                    }
+                    __syncwarp();
+                    const int ix = ix0 + lane;
+                    int64_t i = (int64_t)iy0 * nx + ix;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < kWBPerLane; ++k, i += nx) {
+                        const double *c = T + (k + RAD) * TW + lane + RAD;
+                        const double vi = c[0];
+                        double dx = cmul<P>(RAD, vi), dy = cmul<P>(RAD, vi);
+#pragma unroll
+                        for (int q = 1; q <= RAD; ++q) {
+                            dx = __dadd_rn(__dadd_rn(dx, cmul<P>(RAD + q, c[q])), cmul<P>(RAD - q, c[-q]));
+                            dy = __dadd_rn(__dadd_rn(dy, cmul<P>(RAD + q, c[q * TW])), cmul<P>(RAD - q, c[-q * TW]));
+                        }
+                        const double x = __dsub_rn(__dsub_rn(vi, __dmul_rn(__ldg(gx + i), dx)), __dmul_rn(__ldg(gy + i), dy));
+                        bk[i] = vi;
+                        dst[i] = x;
+                        acc = __dadd_rn(acc, __dmul_rn(kk == 0 ? vi : basis[i], x));
+                    }
+                    acc = warp_sum(acc);
+                    if (lane == 0) pb[wb] = acc;
+                    __syncwarp();   // the tile is restaged for the warp's next patch
+                }
+            } else {
+                for_nodes_red([&](int64_t i, int ix, int iy) {
+                    double bi;
+                    const double x = imsd2d_scaled<P, NX>(src, nx, ix, iy, __ldg(gx + i), __ldg(gy + i), scale, rscale, bi);
+                    bk[i] = bi;
+                    dst[i] = x;
+                    return __dmul_rn(kk == 0 ? bi : basis[i], x);
+                });
+            }
             double *const w = dst;
             double hrun = 0.0;
             for (int j = 0; j <= kk; ++j) {
@@ -1020,8 +1089,12 @@ __global__ void __launch_bounds__(kNT2, 2) gmres2d_coop_ls(Coop2D C) {
             cuda::atomic_ref<unsigned int, cuda::thread_scope_device> ctr(C.bar[slot]);
             ctr.fetch_add(1u, cuda::memory_order_release);
             const unsigned int target = gen * (unsigned int)C.chunks;
-            while (ctr.load(cuda::memory_order_acquire) < target) {
+            // poll relaxed (every acquire load would invalidate the SM's whole L1,
+            // CCTL.IVALL, under the co-resident CTAs that are still gathering taps);
+            // one acquire fence once the last arrival is seen
+            while (ctr.load(cuda::memory_order_relaxed) < target) {
             }
+            cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
         }
         __syncthreads();
     };
