@@ -869,22 +869,10 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                 for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
                     const int by = (int)(wb / pbx);
                     const int ix0 = ((int)(wb - (int64_t)by * pbx)) * 32, iy0 = by * kWBPerLane;
-                    {
-                        // all of the lane's halo loads in flight at once, then the divisions
-                        constexpr int NT = (TW * TH + 31) / 32;
-                        double v[NT];
-#pragma unroll
-                        for (int jt = 0; jt < NT; ++jt) {
-                            const int t = lane + 32 * jt;
-                            const int hy = t / TW, hx = t - hy * TW;
-                            const int gxx = wrapi(ix0 - RAD + hx, nx), gyy = wrapi(iy0 - RAD + hy, nx);
-                            v[jt] = t < TW * TH ? src[(int64_t)gyy * nx + gxx] : 0.0;
-                        }
-#pragma unroll
-                        for (int jt = 0; jt < NT; ++jt) {
-                            const int t = lane + 32 * jt;
-                            if (t < TW * TH) T[t] = div_rcp(v[jt], scale, rscale);
-                        }
+                    for (int t = lane; t < TW * TH; t += 32) {
+                        const int hy = t / TW, hx = t - hy * TW;
+                        const int gxx = wrapi(ix0 - RAD + hx, nx), gyy = wrapi(iy0 - RAD + hy, nx);
+                        T[t] = div_rcp(src[(int64_t)gyy * nx + gxx], scale, rscale);
                     }
                     __syncwarp();
                     const int ix = ix0 + lane;
