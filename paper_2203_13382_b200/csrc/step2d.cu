@@ -693,6 +693,8 @@ struct Coop2D {
     double *part;             // [2][rows_per_round][nwb] reduction partials
     int *flags;               // [rows_per_round][chunks] non-finite rhs
     unsigned int *bar;        // [rows_per_round] per-system barrier counters (zeroed per launch)
+    const double *rhs;        // [B][n] right-hand sides S u computed by a batched SL launch (classic kernel), or NULL
+    const double *rhs_ss;     // [B] their sums of squares
     int32_t *gmres_iters;
     int32_t *status;
 };
@@ -818,9 +820,21 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
         const double *sx = L.s_x + set * n, *sy = L.s_y + set * n;
         const double *gx = L.sig_x + set * n, *gy = L.sig_y + set * n;
         // ---- SL rhs into w, non-finite flag, beta
-        int bad = 0;
         double *src = wping, *dst = wpong;   // Arnoldi vector: read / written by the stencil pass
-        {
+        double beta;
+        int anybad = 0;
+        if (C.rhs) {
+            // the batch's right-hand sides and their norms come from a batched SL
+            // launch of their own (full occupancy, the whole L1 for the taps); the
+            // first stencil pass reads the system's row in place, and the row then
+            // serves as the second Arnoldi buffer
+            src = const_cast<double *>(C.rhs) + b * n;
+            dst = wping;
+            const double ss = C.rhs_ss[b];
+            anybad = !isfinite(ss);     // a non-finite gather value makes the sum non-finite
+            beta = sqrt(ss);
+        } else {
+            int bad = 0;
             const double *u = a.U_in + b * a.ld_in;
             for_nodes_red([&](int64_t i, int ix, int iy) {
                 const double v = sl2d_at<P, NX>(u, nx, __ldg(sx + i), __ldg(sy + i));
@@ -828,16 +842,15 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                 if (!isfinite(v)) bad = 1;
                 return __dmul_rn(v, v);
             });
+            bad = __syncthreads_or(bad);
+            if (tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
+            beta = sqrt(gtotal());
+            if (tid == 0)
+                for (int k = 0; k < C.chunks; ++k) anybad |= C.flags[(int64_t)slot * C.chunks + k];
+            anybad = __syncthreads_or(anybad);
         }
-        bad = __syncthreads_or(bad);
-        if (tid == 0) C.flags[(int64_t)slot * C.chunks + chunk] = bad;
-        const double beta = sqrt(gtotal());
         double *hist = (a.gmres_hist && chunk == 0 && tid == 0) ? a.gmres_hist + b * (int64_t)(K + 1) : nullptr;
         if (hist) hist[0] = beta;
-        int anybad = 0;
-        if (tid == 0)
-            for (int k = 0; k < C.chunks; ++k) anybad |= C.flags[(int64_t)slot * C.chunks + k];
-        anybad = __syncthreads_or(anybad);
         int done = 0;
         const bool skip = anybad || beta == 0.0;
         if (anybad && tid == 0 && chunk == 0) atomicExch(C.status, 1);
@@ -1348,11 +1361,23 @@ static int64_t coop_row_bytes(const mgrit_level_desc *L) {
     return 8 * ((int64_t)(L->gmres_max_iters + 3) * n + (int64_t)kLsVals * nwb) + 4 * 4096 + 8;
 }
 
+// right-hand sides of a corrected batch: a batched SL launch writes rhs_batch()
+// rows S u and their sums of squares ahead of each cooperative launch
+// (128 MB of rows: 16 systems of a 1024^2 mesh, 64 of a 512^2 mesh; at most 256)
+static int64_t rhs_batch(const mgrit_level_desc *L) {
+    const int64_t b = ((int64_t)128 << 20) / (8 * L->n_points);
+    return b < 16 ? 16 : (b > 256 ? 256 : b);
+}
+static int64_t coop_rhs_bytes(const mgrit_level_desc *L) {
+    const int64_t n = L->n_points;
+    return rhs_batch(L) * (8 * n + 8 + 2 * 8 * tiles_for(n)) + 512;
+}
+
 int64_t scratch2d_bytes(const mgrit_level_desc *L, int64_t rows) {
     const int64_t n = L->n_points;
     if (L->kind == MGRIT_KIND_CORRECTED) {
         const int64_t r = rows < 1 ? 1 : rows;
-        return r * coop_row_bytes(L) + 4096;
+        return r * coop_row_bytes(L) + 4096 + coop_rhs_bytes(L);
     }
     // FE needs the SL rows; all kinds need tile partials for row norms
     const int64_t r = rows < 1 ? 1 : rows;
@@ -1444,21 +1469,29 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
         {
             const void *fn = coop_fn(L);
             const int G = coop_capacity(fn);
+            // the classic loop takes its right-hand sides from a batched SL launch when
+            // the scratch holds the batch region (scratch2d_bytes sizes it)
+            static int rhs_on = -1;
+            if (rhs_on < 0) {
+                const char *e = getenv("MGRIT_COOP_RHS_LAUNCH");
+                rhs_on = e ? atoi(e) != 0 : 1;
+            }
+            const bool classic = !(L->gmres_lowsync && L->gmres_max_iters <= kLsMaxK);
+            const int64_t per_row = coop_row_bytes(L);
+            const int64_t rhs_bytes = coop_rhs_bytes(L);
+            const bool rhs_launch = rhs_on && classic && scratch_bytes >= per_row + 4096 + rhs_bytes;
+            const int64_t coop_bytes = rhs_launch ? scratch_bytes - rhs_bytes : scratch_bytes;
             int64_t rows = r.B < G ? r.B : G;
             const int64_t cap = coop_rows_cap(L);
             if (cap > 0 && rows > cap) rows = cap;
-            const int64_t per_row = coop_row_bytes(L);
-            if (scratch_bytes - 4096 < per_row) return (int)MGRIT_EINVAL;
-            if (rows > (scratch_bytes - 4096) / per_row) rows = (scratch_bytes - 4096) / per_row;
+            if (coop_bytes - 4096 < per_row) return (int)MGRIT_EINVAL;
+            if (rows > (coop_bytes - 4096) / per_row) rows = (coop_bytes - 4096) / per_row;
             int chunks = (int)(G / rows);
             if (chunks < 1) chunks = 1;
             while ((int64_t)chunks * rows > 4096) --chunks;
             const int64_t nwb = (n + kWB - 1) / kWB;
             Coop2D C;
             C.L = *L;
-            C.a = a;
-            C.a.partial = r.row_sumsq;
-            C.a.gmres_hist = r.gmres_hist;
             C.rows_per_round = rows;
             C.chunks = chunks;
             C.nwb = nwb;
@@ -1468,18 +1501,49 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             C.part = C.w2 + rows * n;
             C.flags = (int *)(C.part + (int64_t)kLsVals * rows * nwb);
             C.bar = (unsigned int *)(C.flags + rows * chunks);
-            if (cudaMemsetAsync(C.bar, 0, rows * sizeof(unsigned int), st) != cudaSuccess) {
-                set_error("cudaMemsetAsync", cudaGetLastError());
-                return (int)MGRIT_ECUDA;
-            }
-            C.gmres_iters = r.gmres_iters;
             C.status = status;
-            void *args[] = {&C};
-            const int grid = (int)(rows * chunks);
-            cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kNT2, args, 0, st);
-            if (e != cudaSuccess) {
-                set_error("gmres2d_coop", e);
-                return (int)MGRIT_ECUDA;
+            C.rhs = nullptr;
+            C.rhs_ss = nullptr;
+            double *rhs = nullptr, *rhs_ss = nullptr;
+            char *rhs_scr = nullptr;
+            if (rhs_launch) {
+                rhs = (double *)(((uintptr_t)(scr + coop_bytes) + 255) & ~(uintptr_t)255);
+                rhs_ss = rhs + rhs_batch(L) * n;
+                rhs_scr = (char *)(rhs_ss + rhs_batch(L));
+            }
+            const int64_t step = rhs_launch ? rhs_batch(L) : r.B;
+            const int K1 = L->gmres_max_iters + 1;
+            for (int64_t off = 0; off < r.B; off += step) {
+                const int64_t cnt = r.B - off < step ? r.B - off : step;
+                const int64_t *tix = r.t_idx ? r.t_idx + off : nullptr;
+                const int64_t tf = r.t_first + off * r.t_stride;
+                if (rhs_launch) {
+                    mgrit_level_desc Ls = *L;
+                    Ls.kind = MGRIT_KIND_SL;
+                    RowsArgs rr{cnt, tix, tf, r.t_stride, r.U_in + off * r.ld_in, r.ld_in, nullptr, 0, nullptr, 0,
+                                rhs, n, rhs_ss, nullptr};
+                    const int rc2 = apply_rows_2d(&Ls, rr, rhs_scr, 2 * 8 * cnt * tiles_for(n) + 256, status, st);
+                    if (rc2) return rc2;
+                    C.rhs = rhs;
+                    C.rhs_ss = rhs_ss;
+                }
+                C.a = Rows2D{cnt, tix, tf, r.t_stride, r.U_in + off * r.ld_in, r.ld_in,
+                             r.G ? r.G + off * r.ld_g : nullptr, r.ld_g, r.U_sub ? r.U_sub + off * r.ld_sub : nullptr,
+                             r.ld_sub, r.out ? r.out + off * r.ld_out : nullptr, r.ld_out,
+                             r.row_sumsq ? r.row_sumsq + off : nullptr};
+                C.a.gmres_hist = r.gmres_hist ? r.gmres_hist + off * K1 : nullptr;
+                C.gmres_iters = r.gmres_iters ? r.gmres_iters + off : nullptr;
+                if (cudaMemsetAsync(C.bar, 0, rows * sizeof(unsigned int), st) != cudaSuccess) {
+                    set_error("cudaMemsetAsync", cudaGetLastError());
+                    return (int)MGRIT_ECUDA;
+                }
+                void *args[] = {&C};
+                const int grid = (int)(rows * chunks);
+                cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kNT2, args, 0, st);
+                if (e != cudaSuccess) {
+                    set_error("gmres2d_coop", e);
+                    return (int)MGRIT_ECUDA;
+                }
             }
             return check_launch("gmres2d_coop");
         }
