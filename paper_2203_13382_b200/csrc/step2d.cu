@@ -708,7 +708,11 @@ struct CoopSmem {
 template <int P, int NX = 0>
 __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     __shared__ CoopSmem S;
-    __shared__ double s_tile[(kNT2 / 32) * (32 + (P + 1)) * (kWBPerLane + (P + 1))];   // per warp: a patch + halo
+    // per warp: a patch + halo of the normalised vector (stencil pass), and the
+    // Arnoldi vector w of the warp's first patch (its second patch's w reuses
+    // the halo tile, free once that patch's stencil is done)
+    constexpr int kTileElems = (32 + (P + 1)) * (kWBPerLane + (P + 1));
+    extern __shared__ double s_tile[];   // [kNT2 / 32][kTileElems + kWB] (coop_dyn_smem)
     const mgrit_level_desc &L = C.L;
     const Rows2D &a = C.a;
     const int nx = L.n_x;
@@ -738,16 +742,28 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
     // for every node of this CTA's warp blocks, body(i, ix, iy) -> value; the
     // per-warp-block sum (per lane in k order, then the butterfly) goes to the
     // current partial buffer
+    // On-chip w (patch mode, at most two patches per warp): between the stencil
+    // pass of an Arnoldi step and its last projection, w = A b_k lives in the
+    // shared memory of the warp that owns the nodes (slot 0: its own 256
+    // doubles; slot 1: the halo tile), so a projection pass streams only b_j
+    // and b_{j+1} from L2 (16 B per node instead of 32).  wp is that node's
+    // slot, or nullptr when w stays in global memory.
+    const bool onchip = patch && (nwb + C.chunks - 1) / C.chunks <= 2 * NW;
+    double *const Ttile = s_tile + warp * (kTileElems + kWB);
+    double *const Wown = Ttile + kTileElems;
     auto for_nodes_red = [&](auto &&body) {
         double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
-        for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
+        int sl = 0;
+        for (int64_t wb = wb0 + warp; wb < wb1; wb += NW, ++sl) {
             double acc = 0.0;
             if (patch) {
                 const int by = (int)(wb / pbx);
                 const int ix = ((int)(wb - (int64_t)by * pbx)) * 32 + lane;
                 int64_t i = (int64_t)by * kWBPerLane * nx + ix;
+                double *wp = onchip ? (sl == 0 ? Wown : Ttile) + lane : nullptr;
 #pragma unroll
-                for (int k = 0; k < kWBPerLane; ++k, i += nx) acc = __dadd_rn(acc, body(i, ix, by * kWBPerLane + k));
+                for (int k = 0; k < kWBPerLane; ++k, i += nx)
+                    acc = __dadd_rn(acc, body(i, ix, by * kWBPerLane + k, wp ? wp + 32 * k : nullptr));
             } else {
                 const int64_t base = wb * kWB;
                 const int iy0 = row_blocks ? (int)(base / nx) : 0;
@@ -764,7 +780,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                             iy = (int)((unsigned)i / (unsigned)nx);
                             ix = (int)i - iy * nx;
                         }
-                        acc = __dadd_rn(acc, body(i, ix, iy));
+                        acc = __dadd_rn(acc, body(i, ix, iy, (double *)nullptr));
                     }
                 }
             }
@@ -836,7 +852,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
         } else {
             int bad = 0;
             const double *u = a.U_in + b * a.ld_in;
-            for_nodes_red([&](int64_t i, int ix, int iy) {
+            for_nodes_red([&](int64_t i, int ix, int iy, double *wp) {
                 const double v = sl2d_at<P, NX>(u, nx, __ldg(sx + i), __ldg(sy + i));
                 src[i] = v;
                 if (!isfinite(v)) bad = 1;
@@ -877,9 +893,10 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                 // shared memory.  Same b values, same stencil arithmetic as
                 // imsd2d_scaled: identical w.
                 constexpr int RAD = (P + 1) / 2, TW = 32 + 2 * RAD, TH = kWBPerLane + 2 * RAD;
-                double *T = s_tile + warp * (TW * TH);
+                double *T = Ttile;
                 double *pb = C.part + ((int64_t)pbuf * C.rows_per_round + slot) * nwb;
-                for (int64_t wb = wb0 + warp; wb < wb1; wb += NW) {
+                int sl = 0;
+                for (int64_t wb = wb0 + warp; wb < wb1; wb += NW, ++sl) {
                     const int by = (int)(wb / pbx);
                     const int ix0 = ((int)(wb - (int64_t)by * pbx)) * 32, iy0 = by * kWBPerLane;
                     for (int t = lane; t < TW * TH; t += 32) {
@@ -891,6 +908,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                     const int ix = ix0 + lane;
                     int64_t i = (int64_t)iy0 * nx + ix;
                     double acc = 0.0;
+                    double xk[kWBPerLane];
 #pragma unroll
                     for (int k = 0; k < kWBPerLane; ++k, i += nx) {
                         const double *c = T + (k + RAD) * TW + lane + RAD;
@@ -903,15 +921,24 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                         }
                         const double x = __dsub_rn(__dsub_rn(vi, __dmul_rn(__ldg(gx + i), dx)), __dmul_rn(__ldg(gy + i), dy));
                         bk[i] = vi;
-                        dst[i] = x;
+                        if (onchip)
+                            xk[k] = x;
+                        else
+                            dst[i] = x;
                         acc = __dadd_rn(acc, __dmul_rn(kk == 0 ? vi : basis[i], x));
                     }
                     acc = warp_sum(acc);
                     if (lane == 0) pb[wb] = acc;
-                    __syncwarp();   // the tile is restaged for the warp's next patch
+                    __syncwarp();   // every lane is done with the tile: it is restaged for the warp's
+                                    // next patch, or (second patch) takes that patch's w
+                    if (onchip) {
+                        double *wp = (sl == 0 ? Wown : T) + lane;
+#pragma unroll
+                        for (int k = 0; k < kWBPerLane; ++k) wp[32 * k] = xk[k];
+                    }
                 }
             } else {
-                for_nodes_red([&](int64_t i, int ix, int iy) {
+                for_nodes_red([&](int64_t i, int ix, int iy, double *wp) {
                     double bi;
                     const double x = imsd2d_scaled<P, NX>(src, nx, ix, iy, __ldg(gx + i), __ldg(gy + i), scale, rscale, bi);
                     bk[i] = bi;
@@ -937,14 +964,18 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
                 const double *bj = basis + (int64_t)j * n;
                 const double *bn = j < kk ? basis + (int64_t)(j + 1) * n : nullptr;
                 if (bn) {
-                    for_nodes_red([&](int64_t i, int ix, int iy) {
-                        const double x = fma(-h, bj[i], w[i]);
-                        w[i] = x;
+                    for_nodes_red([&](int64_t i, int ix, int iy, double *wp) {
+                        const double x = fma(-h, bj[i], wp ? *wp : w[i]);
+                        if (wp)
+                            *wp = x;
+                        else
+                            w[i] = x;
                         return __dmul_rn(bn[i], x);
                     });
                 } else {
-                    for_nodes_red([&](int64_t i, int ix, int iy) {
-                        const double x = fma(-h, bj[i], w[i]);
+                    for_nodes_red([&](int64_t i, int ix, int iy, double *wp) {
+                        // last projection: w goes to memory for the next stencil pass
+                        const double x = fma(-h, bj[i], wp ? *wp : w[i]);
                         w[i] = x;
                         return __dmul_rn(x, x);
                     });
@@ -985,7 +1016,7 @@ __global__ void __launch_bounds__(kNT2, 4) gmres2d_coop(Coop2D C) {
             }
         }
         __syncthreads();
-        for_nodes_red([&](int64_t i, int ix, int iy) {
+        for_nodes_red([&](int64_t i, int ix, int iy, double *wp) {
             double x = 0.0;
             if (anybad) {
                 x = __longlong_as_double(0x7ff8000000000000LL);
@@ -1322,12 +1353,26 @@ static const void *coop_fn(const mgrit_level_desc *L) {
     }
 }
 
+// dynamic shared memory of the classic cooperative kernel: per warp a patch +
+// halo tile and one patch of w (gmres2d_coop); the low-sync kernel uses none
+static int coop_dyn_smem(const mgrit_level_desc *L) {
+    if (L->gmres_lowsync && L->gmres_max_iters <= kLsMaxK) return 0;
+    const int tile = (32 + (L->p + 1)) * (kWBPerLane + (L->p + 1));
+    return (kNT2 / 32) * (tile + kWB) * (int)sizeof(double);
+}
+
+// opt in to > 48 KB of dynamic shared memory (cheap and idempotent)
+static void coop_prepare(const void *fn, int smem) {
+    if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
 // systems the corrected 2D kernel keeps in flight: the L2-sized cap (never
 // more than the cooperative grid holds), so callers size scratch for exactly
 // the rows apply_rows_2d uses
 int64_t capacity2d(const mgrit_level_desc *L) {
     if (L->kind != MGRIT_KIND_CORRECTED) return (int64_t)1 << 30;
-    const int64_t g = coop_capacity(coop_fn(L));
+    coop_prepare(coop_fn(L), coop_dyn_smem(L));
+    const int64_t g = coop_capacity(coop_fn(L), coop_dyn_smem(L));
     const int64_t cap = coop_rows_cap(L);
     return cap > 0 && cap < g ? cap : g;
 }
@@ -1468,7 +1513,9 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
     if (L->kind == MGRIT_KIND_CORRECTED) {
         {
             const void *fn = coop_fn(L);
-            const int G = coop_capacity(fn);
+            const int smem = coop_dyn_smem(L);
+            coop_prepare(fn, smem);
+            const int G = coop_capacity(fn, smem);
             // the classic loop takes its right-hand sides from a batched SL launch when
             // the scratch holds the batch region (scratch2d_bytes sizes it)
             static int rhs_on = -1;
@@ -1539,7 +1586,7 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
                 }
                 void *args[] = {&C};
                 const int grid = (int)(rows * chunks);
-                cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kNT2, args, 0, st);
+                cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kNT2, args, smem, st);
                 if (e != cudaSuccess) {
                     set_error("gmres2d_coop", e);
                     return (int)MGRIT_ECUDA;
