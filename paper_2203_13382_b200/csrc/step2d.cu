@@ -1333,7 +1333,7 @@ int dispatch_p(int p, Fn &&f) {
 
 }  // namespace
 
-static int64_t coop_rows_cap(const mgrit_level_desc *L);
+static int64_t coop_rows_cap(const mgrit_level_desc *L, int64_t grid);
 
 // the cooperative GMRES instantiation a level dispatches to: p = 3 on the
 // 512-wide mesh and p = 5 on the 1024-wide mesh use compile-time row strides
@@ -1373,7 +1373,7 @@ int64_t capacity2d(const mgrit_level_desc *L) {
     if (L->kind != MGRIT_KIND_CORRECTED) return (int64_t)1 << 30;
     coop_prepare(coop_fn(L), coop_dyn_smem(L));
     const int64_t g = coop_capacity(coop_fn(L), coop_dyn_smem(L));
-    const int64_t cap = coop_rows_cap(L);
+    const int64_t cap = coop_rows_cap(L, g);
     return cap > 0 && cap < g ? cap : g;
 }
 
@@ -1383,7 +1383,7 @@ int64_t capacity2d(const mgrit_level_desc *L) {
 // rather than HBM (measured on B200: cfg4 64 -> 8 systems 679 -> 618 ms,
 // cfg5 32 -> 2 systems 4381 -> 3988 ms per solve).  MGRIT_COOP_ROWS
 // overrides (0 = as many as the resident grid allows).
-static int64_t coop_rows_cap(const mgrit_level_desc *L) {
+static int64_t coop_rows_cap(const mgrit_level_desc *L, int64_t grid = 0) {
     static int64_t env = -2;
     if (env == -2) {
         const char *e = getenv("MGRIT_COOP_ROWS");
@@ -1393,9 +1393,23 @@ static int64_t coop_rows_cap(const mgrit_level_desc *L) {
     int dev = 0, l2 = 126 << 20;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-    const int vecs = L->gmres_max_iters + 2 < 6 ? L->gmres_max_iters + 2 : 6;
+    const bool classic = !(L->gmres_lowsync && L->gmres_max_iters <= kLsMaxK);
+    // classic loop on a patch-mapped mesh: w lives on chip and the right-hand
+    // sides in their own rows, so a system's L2 working set is ~5 vectors; but
+    // never so many systems that a warp would own more than two patches
+    // (on-chip w needs <= 16 patches per CTA): measured on cfg4, 9 systems in
+    // flight 392 ms, 8: 401 ms, 6: 444 ms per solve
+    const bool onchip = classic && (L->n_x % 32) == 0;
+    const int wv = onchip ? 5 : 6;
+    const int vecs = L->gmres_max_iters + 2 < wv ? L->gmres_max_iters + 2 : wv;
     const int64_t per = (int64_t)vecs * L->n_points * 8;
-    const int64_t r = (int64_t)(0.8 * (double)l2) / (per > 0 ? per : 1);
+    int64_t r = (int64_t)(0.8 * (double)l2) / (per > 0 ? per : 1);
+    if (onchip && grid > 0) {
+        const int64_t nwb = (L->n_points + kWB - 1) / kWB;
+        const int64_t min_chunks = (nwb + 2 * (kNT2 / 32) - 1) / (2 * (kNT2 / 32));
+        const int64_t lim = grid / (min_chunks > 0 ? min_chunks : 1);
+        if (lim >= 1 && r > lim) r = lim;
+    }
     return r < 1 ? 1 : r;
 }
 
@@ -1529,7 +1543,7 @@ int apply_rows_2d(const mgrit_level_desc *L, const RowsArgs &r, void *scratch, i
             const bool rhs_launch = rhs_on && classic && scratch_bytes >= per_row + 4096 + rhs_bytes;
             const int64_t coop_bytes = rhs_launch ? scratch_bytes - rhs_bytes : scratch_bytes;
             int64_t rows = r.B < G ? r.B : G;
-            const int64_t cap = coop_rows_cap(L);
+            const int64_t cap = coop_rows_cap(L, G);
             if (cap > 0 && rows > cap) rows = cap;
             if (coop_bytes - 4096 < per_row) return (int)MGRIT_EINVAL;
             if (rows > (coop_bytes - 4096) / per_row) rows = (coop_bytes - 4096) / per_row;
