@@ -499,7 +499,8 @@ def _rooflines(args, cfg, levels, breakdown, clk_summary):
     elif cfg.dim == 1:
         limiter = "latency: MGS-GMRES reduction chain of a few row chains (see DESIGN.md section 4)"
     else:
-        limiter = "per-system barriers + L2-resident Krylov passes of the cooperative GMRES (DESIGN.md section 4)"
+        limiter = ("Krylov passes of the cooperative GMRES through L2/HBM with two systems in flight, ~17 dependent "
+                   "pass + barrier intervals per system (DESIGN.md section 4, profiles/r02g_probe_coop2d_cfg5mesh_k4.txt)")
     total = sum(v["ms_avg"] * v["launches"] for v in breakdown.values())
     roofline = {"bound": "hbm", "limiter": limiter, "kernel": top, "achieved": round(achieved, 1),
                 "peak": peak["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peak["hbm_gbs"], 4),
